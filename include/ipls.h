@@ -1,0 +1,144 @@
+/*
+ * ipls.h — C ABI of the B200 (sm_100a) IPLS distribution-step library, libipls.so.
+ *
+ * Paper: "In-Place Parallel Learned Sort" (IPLS), arXiv 2208.06902; the reference text is
+ * PAPER.md, cited here as P:<line>.  Readings of the paper where it is silent or ambiguous
+ * are numbered R<n> and listed in DESIGN.md §3.
+ *
+ * Conventions for every entry point:
+ *  - d_* arguments are CUDA device pointers, h_* arguments host pointers.  Keys are 64-bit
+ *    words: IEEE binary64 (IPLS_KEY_F64) or unsigned 64-bit integers (IPLS_KEY_U64),
+ *    8-byte aligned, contiguous.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Work is
+ *    stream-ordered; every call synchronises `stream` once before returning so it can
+ *    return a status (timing with events must bracket the call).
+ *  - No exceptions cross the ABI; errors are returned as ipls_status.  On any error other
+ *    than IPLS_ERR_CUDA the caller's key array is left unmodified.
+ *  - Thread safety: concurrent calls on different streams are safe; the library keeps one
+ *    internal workspace per stream (guarded by a mutex) unless the caller passes its own.
+ *  - Ordering: keys are sorted by the ordering key of P:576 (the float -> integer map):
+ *    numeric order for doubles with -0.0 before +0.0; NaN is rejected (R0).
+ */
+#ifndef IPLS_H
+#define IPLS_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  IPLS_OK = 0,
+  IPLS_ERR_INVALID_ARGUMENT = 1, /* null pointer with n > 0, k < 3 or k > IPLS_MAX_K, ... */
+  IPLS_ERR_NAN_KEY = 2,          /* a float64 key is NaN; the array is left unmodified  */
+  IPLS_ERR_DEGENERATE_SAMPLE = 3,/* ipls_fit_fmcd only: Listing 1 gave no usable model */
+  IPLS_ERR_OUT_OF_MEMORY = 4,    /* device allocation or caller workspace too small     */
+  IPLS_ERR_CUDA = 5,             /* a CUDA runtime error (see ipls_last_cuda_error)      */
+  IPLS_ERR_NOT_IMPLEMENTED = 6
+} ipls_status;
+
+typedef enum { IPLS_KEY_F64 = 0, IPLS_KEY_U64 = 1 } ipls_key_type;
+
+/* Partition model kinds.  LINEAR: F(x) = clamp(floor(a*x + b), 0, k-1) with
+ * (a, b) from FMCD (Listing 1).  EQ3: equality split into <pivot, ==pivot,
+ * >pivot by ordering key (IPS4o equality buckets; used for degenerate samples, R5). */
+typedef enum { IPLS_MODEL_LINEAR = 0, IPLS_MODEL_EQ3 = 1 } ipls_model_kind;
+
+#define IPLS_MAX_K 1024u          /* fan-out limit of the sm_100a kernels (smem-resident) */
+#define IPLS_MAX_BASE_CASE 4096u  /* base-case limit (n <= 2^12)                    */
+#define IPLS_DEFAULT_SEED 0x49504C53ull
+
+typedef struct {
+  uint32_t k;         /* buckets per level, 3..IPLS_MAX_K (P:473 uses 256)                 */
+  uint32_t base_case; /* segments of <= base_case keys go to the base case, 1..4096 */
+  uint64_t seed;      /* sampling seed (R18)                                               */
+  uint32_t flags;     /* reserved, must be 0                                               */
+} ipls_config;
+
+typedef struct {
+  double a, b;        /* LINEAR: slope A and intercept B of Listing 1 (0 for EQ3)          */
+  uint32_t k;         /* bucket count the model was fitted for (k_eff = 3 for EQ3)         */
+  uint32_t D;         /* FMCD conflict degree (0 for EQ3)                                   */
+  uint32_t kind;      /* ipls_model_kind                                                    */
+  uint32_t capped;    /* 1 if Listing 1 stopped at D*3 > N (R4)                             */
+  uint64_t pivot_ok;  /* EQ3: ordering key of the pivot (0 for LINEAR)                      */
+} ipls_model;
+
+/* Default configuration: k = 256, base_case = 4096, seed = IPLS_DEFAULT_SEED. */
+ipls_config ipls_default_config(void);
+
+/* Sort n keys in place on the device (P:114-121 recursion, P:469-475 IPLS parameters).
+ * d_keys: device array of n keys, caller-owned.  Uses an internal workspace (8n bytes of
+ * scratch plus metadata, see ipls_workspace_bytes) cached per stream.
+ * n == 0 or 1: IPLS_OK without touching memory.  Errors: INVALID_ARGUMENT (d_keys NULL
+ * with n > 0, n > 2^32-1), NAN_KEY (array unmodified), OUT_OF_MEMORY, CUDA. */
+ipls_status ipls_sort_f64(double* d_keys, size_t n, void* stream);
+ipls_status ipls_sort_u64(uint64_t* d_keys, size_t n, void* stream);
+
+/* As above with an explicit key type and configuration.  d_workspace may be NULL (internal
+ * cache) or a device buffer of at least ipls_workspace_bytes(n, t, cfg) bytes, which the
+ * call owns for its duration.  cfg NULL = ipls_default_config(). */
+ipls_status ipls_sort_ex(void* d_keys, size_t n, ipls_key_type t, const ipls_config* cfg,
+                         void* d_workspace, size_t ws_bytes, void* stream);
+
+/* Device workspace ipls_sort_ex needs: one n-key scratch buffer (8n bytes; the ping-pong
+ * target that replaces IPS4o's in-place block permutation) plus per-level
+ * metadata bounded by n, k and base_case. */
+size_t ipls_workspace_bytes(size_t n, ipls_key_type t, const ipls_config* cfg);
+
+/* End-to-end variant: h_keys is a HOST array (ideally pinned); the call copies it to the
+ * device, sorts, and copies the result back, all on `stream`. */
+ipls_status ipls_sort_host(void* h_keys, size_t n, ipls_key_type t, const ipls_config* cfg,
+                           void* stream);
+
+/* FMCD fit (Listing 1, binary64, R3/R4) of one already-sorted sample.
+ * d_sorted_sample: S keys of type t sorted by ordering key (device).  S >= 4, 3 <= k <=
+ * IPLS_MAX_K, S <= 65536.  Writes *h_out.  Returns IPLS_ERR_DEGENERATE_SAMPLE (with
+ * h_out->kind = EQ3 and pivot_ok = ordering key of s[S/2]) when !(u_d > 0) or A, B are not
+ * finite (R5). */
+ipls_status ipls_fit_fmcd(const void* d_sorted_sample, size_t S, ipls_key_type t, uint32_t k,
+                          ipls_model* h_out, void* stream);
+
+/* One distribution step of a single segment with a caller-supplied model: classify every
+ * key (evaluated as RN(RN(a*x) + b), no FMA, R7), histogram, prefix-sum and
+ * stable scatter into contiguous buckets (R11).
+ * d_in, d_out: n keys each (device, must not overlap).  d_offsets: k_eff+1 uint64 bucket
+ * boundaries (device).  d_bucket_ids: nullable; n uint16 per-key buckets in input order. */
+ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_key_type t,
+                                 const ipls_model* h_model, uint64_t* d_offsets,
+                                 uint16_t* d_bucket_ids, void* stream);
+
+/* ---- trace (tests and diagnostics) ---- */
+typedef struct {
+  uint32_t level, kind;     /* level of the recursion; ipls_model_kind                      */
+  uint64_t begin, m, S;     /* segment [begin, begin+m) and its sample size                  */
+  double a, b;              /* model (0 for EQ3)                                             */
+  uint32_t D, capped;       /* FMCD outputs (0 for EQ3)                                      */
+  uint64_t pivot_ok;        /* EQ3 pivot (0 for LINEAR)                                      */
+  uint32_t k_eff, requeued; /* children count; 1 if re-queued by the no-progress guard (R10) */
+} ipls_segment_record;
+
+typedef struct {
+  ipls_segment_record* records; size_t records_cap; size_t records_len; /* host, out       */
+  uint64_t* counts; size_t counts_cap; size_t counts_len;  /* host: k_eff per record, out  */
+  uint64_t* samples; size_t samples_cap; size_t samples_len; /* host: sorted sample bits  */
+  void* d_snapshots;        /* device, nullable: snapshot_levels * n keys, array after level L */
+  uint32_t snapshot_levels;
+  uint32_t levels;          /* out: number of partition levels run                           */
+} ipls_trace;
+
+/* ipls_sort_ex plus a per-segment trace, records ordered by (level, begin).  Arrays that
+ * are too small are filled up to their capacity and *_len reports the full size. */
+ipls_status ipls_sort_trace(void* d_keys, size_t n, ipls_key_type t, const ipls_config* cfg,
+                            ipls_trace* trace, void* stream);
+
+const char* ipls_status_string(ipls_status s);
+const char* ipls_last_cuda_error(void);
+/* Number of kernels the library enqueued since load (diagnostics / bench launch count). */
+uint64_t ipls_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,158 @@
+// ipls_device.cuh — device primitives of the sm_100a IPLS path.
+//
+// Key domains (R0, R17): a key is a raw 64-bit word.  Its ordering key `ok` is the
+// order-preserving unsigned image (doubles: flip all bits of negatives, set the sign bit of
+// non-negatives; u64: identity) and its model value `v` is the double itself or the u64
+// converted round-to-nearest.  The partition model is evaluated as two separately
+// rounded operations, y = RN(RN(a*v) + b), written with __dmul_rn/__dadd_rn so that no FMA
+// contraction can change a bucket (R7).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ipls {
+
+constexpr uint32_t kModelLinear = 0;
+constexpr uint32_t kModelEq3 = 1;
+constexpr uint32_t kSegForceEq3 = 1u;
+constexpr uint64_t kDstUserBit = 1ull << 63;  // seg_dst encoding: buffer select
+constexpr uint32_t kInhBit = 1u << 31;        // count word: child not homogeneous
+
+struct SegDesc {            // one partition work item of a level (segment of the array)
+  uint64_t begin;           // absolute position of the segment
+  uint32_t m;               // keys in the segment (> base case, or requeued)
+  uint32_t S;               // sample size S(m) (R1, R19)
+  uint64_t sample_off;      // offset of its sample in the level's sample buffer
+  uint32_t chunk_first, nchunks;
+  uint32_t unit_first, nunits;
+  uint32_t flags;           // kSegForceEq3
+  uint32_t pad;
+};
+
+struct ModelDev {           // fitted model of one segment (Listing 1 outputs or EQ3)
+  double A, B;
+  uint64_t pivot_ok;
+  uint32_t kind, D, capped, k_eff;
+};
+
+struct ChunkDesc {          // a run of <= CHUNK keys of one segment, processed by one CTA
+  uint64_t start;
+  uint32_t len, seg;
+};
+
+struct UnitDesc {           // up to 32 consecutive chunks of one segment (column-scan unit)
+  uint32_t seg, chunk_first, nch, pad;
+};
+
+struct Window {             // contiguous run of whole final segments for the base case
+  uint64_t begin;
+  uint32_t len, buf;        // buf: 0 = user array, 1 = scratch
+};
+
+struct Fill {               // homogeneous child that must be written into the user array
+  uint64_t begin;
+  uint64_t value;
+  uint32_t len, pad;
+};
+
+struct LevelCounters {      // device-side counters of the level being built
+  uint32_t n_segs, n_chunks, n_units, n_samples;
+  uint32_t n_windows, n_fills, err, pad;
+  uint64_t keys;            // keys in next-level segments
+};
+
+constexpr uint32_t kErrNan = 1u;
+constexpr uint32_t kErrOverflow = 2u;
+
+__device__ __forceinline__ uint64_t ok_of_f64(uint64_t bits) {
+  return (bits >> 63) ? ~bits : (bits | (1ull << 63));
+}
+template <bool F64>
+__device__ __forceinline__ uint64_t ok_of(uint64_t bits) {
+  if constexpr (F64) return ok_of_f64(bits); else return bits;
+}
+template <bool F64>
+__device__ __forceinline__ uint64_t bits_of_ok(uint64_t ok) {
+  if constexpr (F64) return (ok >> 63) ? (ok & ~(1ull << 63)) : ~ok; else return ok;
+}
+template <bool F64>
+__device__ __forceinline__ double value_of(uint64_t bits) {
+  if constexpr (F64) return __longlong_as_double((long long)bits);
+  else return __ull2double_rn(bits);
+}
+__device__ __forceinline__ bool is_nan_bits(uint64_t bits) {
+  return ((bits >> 52) & 0x7ff) == 0x7ff && (bits & 0xfffffffffffffull) != 0;
+}
+
+// P:394-402 with R7: 0 if !(y >= 0); k-1 if y >= k; floor(y) otherwise.
+__device__ __forceinline__ uint32_t linear_bucket(double v, double A, double B, double kd,
+                                                  uint32_t km1) {
+  double t = __dmul_rn(A, v);
+  double y = __dadd_rn(t, B);
+  if (!(y >= 0.0)) return 0u;
+  if (y >= kd) return km1;
+  return (uint32_t)y;  // cvt.rzi: 0 <= y < k so truncation == floor
+}
+
+template <bool F64>
+__device__ __forceinline__ uint32_t bucket_of(uint64_t bits, const ModelDev& md, double kd,
+                                              uint32_t km1) {
+  if (md.kind == kModelEq3) {
+    uint64_t o = ok_of<F64>(bits);
+    return (o < md.pivot_ok) ? 0u : ((o == md.pivot_ok) ? 1u : 2u);
+  }
+  return linear_bucket(value_of<F64>(bits), md.A, md.B, kd, km1);
+}
+
+// SplitMix64 output function (R18).
+__device__ __forceinline__ uint64_t sm64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// S(m) = min(max(ceil(ceil(log2 m)/5) k - 1, 4), floor(m/2))   (R1, R19)
+__host__ __device__ __forceinline__ uint32_t sample_size(uint64_t m, uint32_t k) {
+  uint32_t lg = 0;
+  for (uint64_t x = (m > 0 ? m - 1 : 0); x; x >>= 1) ++lg;
+  uint64_t S = (uint64_t)((lg + 4) / 5) * k;
+  S = S ? S - 1 : 0;
+  if (S < 4) S = 4;
+  if (S > m / 2) S = m / 2;
+  return (uint32_t)S;
+}
+
+// ---- block-wide exclusive scan of one uint32 per thread (blockDim multiple of 32) ----
+template <int NT>
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t* s_warp,
+                                                          uint32_t* total) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_warp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = (lane < NW) ? s_warp[lane] : 0u;
+    uint32_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    if (lane < NW) s_warp[lane] = ti - t;
+    if (lane == NW - 1) s_warp[NW] = ti;
+  }
+  __syncthreads();
+  uint32_t res = s_warp[w] + inc - x;
+  if (total) *total = s_warp[NW];
+  __syncthreads();
+  return res;
+}
+
+}  // namespace ipls

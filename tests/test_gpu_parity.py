@@ -1,0 +1,304 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Bit-exact everywhere: FMCD coefficients (A, B bits), D, kind, pivot, per-key bucket ids,
+bucket counts, per-level layouts and the final array.
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2208_06902_b200 import datagen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def ipls():
+    import paper_2208_06902_b200 as m
+    assert torch.cuda.is_available()
+    m.lib()
+    return m
+
+
+def dev(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64).copy()).cuda()
+
+
+def host(t, dtype):
+    return t.cpu().numpy().view(dtype)
+
+
+def kt_of(a):
+    return 0 if a.dtype == np.float64 else 1
+
+
+def ok_sorted_sample(a, idx):
+    s = a[idx.astype(np.int64)]
+    return s[np.argsort(oracle.ordering_keys(s), kind="stable")]
+
+
+# ---------------------------------------------------------------- FMCD (K2) ----------
+def fit_cases():
+    rng = np.random.default_rng(11)
+    cases = []
+    for t in range(60):
+        S = int(rng.choice([4, 5, 17, 100, 1023, 3071, 4095, 6143, 7167, 8192]))
+        k = int(rng.choice([3, 4, 10, 256, 1024]))
+        dist = ["normal", "lognormal", "uniform", "ints", "dups", "const", "sorted_i",
+                "u64"][t % 8]
+        if dist == "normal":
+            a = rng.normal(0, 1, S)
+        elif dist == "lognormal":
+            a = rng.lognormal(0, 2, S)
+        elif dist == "uniform":
+            a = rng.random(S)
+        elif dist == "ints":
+            a = rng.integers(0, 50, S).astype(np.float64)
+        elif dist == "dups":
+            a = np.where(rng.random(S) < 0.9, 1.0, rng.normal(0, 1, S))
+        elif dist == "const":
+            a = np.full(S, -2.5)
+        elif dist == "sorted_i":
+            a = np.arange(S, dtype=np.float64)
+        else:
+            a = rng.integers(0, 2 ** 64 - 1, S, dtype=np.uint64, endpoint=True)
+        cases.append((a, k))
+    return cases
+
+
+@pytest.mark.parametrize("case", range(60))
+def test_fit_fmcd_parity(ipls, case):
+    a, k = fit_cases()[case]
+    s = a[np.argsort(oracle.ordering_keys(a), kind="stable")]
+    m = ipls.fit_fmcd(dev(s), k, key_type=kt_of(s))
+    if s.size < 4:
+        return
+    o = oracle.fit_fmcd(s.astype(np.float64), k)
+    assert m.degenerate == o.degenerate
+    if o.degenerate:
+        assert m.kind == ipls.MODEL_EQ3
+        assert m.pivot_ok == int(oracle.ordering_keys(s[s.size // 2:s.size // 2 + 1])[0])
+    else:
+        assert (m.D, bool(m.capped)) == (o.D, o.capped)
+        assert m.a == o.A and m.b == o.B  # bit-exact binary64
+
+
+# ---------------------------------------------------------- partition (K3..K4) -------
+def test_partition_worked_example(ipls, golden):
+    g = golden("worked_example.txt")
+    x = np.array([float(v) for v in g["input"][0]])
+    mdl = ipls.Model(0.15, -1.55, 4, 0, ipls.MODEL_LINEAR, 0, 0)
+    out = torch.empty(x.size, dtype=torch.int64, device="cuda")
+    off, ids = ipls.partition_level(dev(x), out, mdl, key_type=0, want_ids=True)
+    assert host(out, np.float64).tolist() == [float(v) for v in g["contiguous"][0]]
+    assert off.cpu().tolist() == [0, 7, 9, 13, 20]
+    assert ids.cpu().numpy().tolist() == [1, 3, 3, 2, 2, 3, 0, 2, 3, 0, 3, 3, 0, 0, 3, 0, 0, 0,
+                                          1, 2]
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 31, 4095, 4096, 4097, 65536 * 3 + 17, 1_000_003])
+@pytest.mark.parametrize("dist", ["normal", "lognormal", "dups", "u64"])
+@pytest.mark.parametrize("k", [3, 256, 1024])
+def test_partition_level_parity(ipls, n, dist, k):
+    rng = np.random.default_rng(n * 7 + k)
+    if dist == "normal":
+        a = rng.normal(0, 1, n)
+    elif dist == "lognormal":
+        a = rng.lognormal(0, 2, n)
+    elif dist == "dups":
+        a = rng.integers(0, 7, n).astype(np.float64)
+    else:
+        a = rng.integers(0, 2 ** 64 - 1, n, dtype=np.uint64, endpoint=True)
+    if n >= 8:
+        S = min(oracle.sample_size(n, k), 8192)
+        idx = oracle.sample_positions(oracle.DEFAULT_SEED, 0, 0, n, S)
+        fit = oracle.fit_fmcd(ok_sorted_sample(a, idx).astype(np.float64), k)
+    else:
+        fit = oracle.Fit(1.0, 0.0, 1, False, False)
+    if fit.degenerate or k == 3:
+        piv = int(oracle.ordering_keys(a[n // 2:n // 2 + 1])[0]) if n else 0
+        kind, A, B, kk = oracle.MODEL_EQ3, 0.0, 0.0, 3
+    else:
+        kind, A, B, kk = oracle.MODEL_LINEAR, fit.A, fit.B, k
+        piv = 0
+    want, woff, wids = oracle.partition(a, A, B, kk, kind=kind, pivot_ok=piv)
+    mdl = ipls.Model(A, B, kk, 0, kind, 0, piv)
+    out = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")[:n]
+    off, ids = ipls.partition_level(dev(a), out, mdl, key_type=kt_of(a), want_ids=True)
+    assert np.array_equal(off.cpu().numpy().astype(np.uint64), woff)
+    assert host(out, a.dtype).tobytes() == want.tobytes()
+    assert np.array_equal(ids.cpu().numpy().view(np.uint16), wids)
+
+
+# ------------------------------------------------------------- whole sort ------------
+def compare_traces(gtr, ores):
+    assert gtr.levels == ores.levels
+    assert len(gtr.records) == len(ores.records)
+    for g, o in zip(gtr.records, ores.records):
+        assert (g.level, g.begin, g.m, g.S) == (o.level, o.begin, o.m, o.S)
+        assert (g.kind, g.D, g.capped, g.pivot_ok, g.k_eff, g.requeued) == \
+            (o.kind, o.D, o.capped, o.pivot_ok, o.k_eff, o.requeued)
+        assert g.A == o.A and g.B == o.B
+        assert np.array_equal(g.counts, o.counts)
+        assert np.array_equal(g.sample, o.sample)
+
+
+FUZZ_SIZES = [(2, 4, 1), (9, 4, 2), (100, 4, 9), (5000, 16, 64), (70_001, 256, 4096),
+              (300_000, 1024, 4096), (200_000, 64, 100)]
+
+
+@pytest.mark.parametrize("kind", datagen.FUZZ_KINDS)
+@pytest.mark.parametrize("size", range(len(FUZZ_SIZES)))
+def test_sort_parity_fuzz(ipls, kind, size):
+    n, k, B = FUZZ_SIZES[size]
+    rng = np.random.default_rng(size * 131 + len(kind))
+    a = datagen.fuzz_array(rng, n, kind)
+    want = a.copy()
+    ores = oracle.sort(want, k=k, base_case=B, trace=True, snapshots=True)
+    t = dev(a)
+    gtr = ipls.sort_trace(t, k=k, base_case=B, key_type=kt_of(a),
+                          snapshot_levels=max(1, ores.levels))
+    assert host(t, a.dtype).tobytes() == want.tobytes()
+    compare_traces(gtr, ores)
+    for lv in range(ores.levels):
+        assert np.array_equal(gtr.snapshots[lv].cpu().numpy().view(np.uint64),
+                              ores.snapshots[lv]), f"layout after level {lv} differs"
+
+
+def test_worked_example_sort(ipls, golden):
+    x = np.array([float(v) for v in golden("worked_example.txt")["input"][0]])
+    t = dev(x)
+    want = x.copy()
+    ores = oracle.sort(want, k=4, base_case=9, trace=True)
+    gtr = ipls.sort_trace(t, k=4, base_case=9, key_type=0)
+    assert host(t, np.float64).tolist() == [float(v) for v in golden("worked_example.txt")["sorted"][0]]
+    compare_traces(gtr, ores)
+
+
+@pytest.mark.parametrize("name,n", [("C1", None), ("C2", 2_000_000), ("C3", 2_000_000),
+                                    ("C4", 2_000_000), ("C5", 3_000_000)])
+def test_configs_scaled_full_trace(ipls, name, n):
+    cfg = datagen.CONFIGS[name]
+    a = datagen.generate(name, n)
+    want = a.copy()
+    ores = oracle.sort(want, k=cfg.k, base_case=cfg.base_case, trace=True)
+    t = dev(a)
+    gtr = ipls.sort_trace(t, k=cfg.k, base_case=cfg.base_case, key_type=kt_of(a))
+    assert host(t, a.dtype).tobytes() == want.tobytes()
+    compare_traces(gtr, ores)
+
+
+def load_oracle_digests():
+    lv, fin = {}, {}
+    with open(os.path.join(GOLD, "oracle_digests.txt")) as f:
+        for line in f:
+            tok = line.split()
+            if not tok or tok[0].startswith("#"):
+                continue
+            if tok[0] == "LEVEL":
+                lv.setdefault(tok[1], []).append((int(tok[2]), int(tok[3]), tok[4], tok[5], tok[6]))
+            elif tok[0] == "FINAL":
+                fin[tok[1]] = (int(tok[2]), tok[3])
+    return lv, fin
+
+
+def gpu_digests(records):
+    by = {}
+    for r in records:
+        by.setdefault(r.level, []).append(r)
+    out = []
+    for lv in sorted(by):
+        rs = sorted(by[lv], key=lambda r: r.begin)
+        h1, h2, h3 = hashlib.sha256(), hashlib.sha256(), hashlib.sha256()
+        for r in rs:
+            orec = oracle.Record(r.level, r.kind, r.begin, r.m, r.S, r.A, r.B, r.D, r.capped,
+                                 r.pivot_ok, r.k_eff, r.requeued, r.sample, r.counts)
+            h1.update(orec.packed())
+            h2.update(r.counts.astype("<u8").tobytes())
+            h3.update(r.sample.astype("<u8").tobytes())
+        out.append((lv, len(rs), h1.hexdigest()[:16], h2.hexdigest()[:16], h3.hexdigest()[:16]))
+    return out
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_configs_full_size_vs_oracle_digests(ipls, name):
+    """Full BASELINE sizes, launched exactly as bench.py times them: every level's records,
+    counts and samples, and the final array, against digests written by the oracle."""
+    lvd, fin = load_oracle_digests()
+    cfg = datagen.CONFIGS[name]
+    a = datagen.generate(name)
+    t = dev(a)
+    del a
+    gtr = ipls.sort_trace(t, k=cfg.k, base_case=cfg.base_case, key_type=kt_of(datagen.generate(name, 1)))
+    assert gpu_digests(gtr.records) == lvd[name]
+    assert gtr.levels == fin[name][0]
+    h = hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()
+    assert h == fin[name][1]
+    # and the untraced entry point (the one bench.py times) gives the same bytes
+    b = datagen.generate(name)
+    t2 = dev(b)
+    ipls.sort(t2, k=cfg.k, base_case=cfg.base_case, key_type=kt_of(b))
+    assert torch.equal(t, t2)
+
+
+def test_nan_rejected_unmodified(ipls):
+    rng = np.random.default_rng(0)
+    for n in (10, 5000, 300_000):
+        a = rng.normal(0, 1, n)
+        a[n // 3] = np.nan
+        t = dev(a)
+        with pytest.raises(ipls.IPLSError) as e:
+            ipls.sort(t, k=256, base_case=4096, key_type=0)
+        assert e.value.status == 2
+        assert host(t, np.float64).tobytes() == a.tobytes()
+
+
+def test_trivial_sizes_and_args(ipls):
+    t = torch.empty(0, dtype=torch.int64, device="cuda")
+    ipls.sort(t, key_type=0)
+    t = dev(np.array([3.5]))
+    ipls.sort(t, key_type=0)
+    assert host(t, np.float64).tolist() == [3.5]
+    with pytest.raises(ipls.IPLSError):
+        ipls.sort(dev(np.zeros(100)), k=2, key_type=0)
+    with pytest.raises(ipls.IPLSError):
+        ipls.sort(dev(np.zeros(100)), k=2048, key_type=0)
+
+
+def test_sort_host_e2e(ipls):
+    a = datagen.generate("C2", 3_000_000)
+    want = np.sort(a)
+    h = torch.from_numpy(a.copy()).pin_memory()
+    ipls.sort_host_ptr(h.data_ptr(), h.numel(), ipls.KEY_F64, k=1024, base_case=4096)
+    torch.cuda.synchronize()
+    assert h.numpy().tobytes() == want.tobytes()
+
+
+def test_caller_workspace(ipls):
+    a = datagen.generate("C3", 1_000_000)
+    want = np.sort(a)
+    t = dev(a)
+    wb = ipls.workspace_bytes(a.size, ipls.KEY_F64, k=1024, base_case=4096)
+    ws = torch.empty(wb, dtype=torch.uint8, device="cuda")
+    ipls.sort(t, k=1024, base_case=4096, key_type=0, workspace=ws)
+    assert host(t, np.float64).tobytes() == want.tobytes()
+    small = torch.empty(1024, dtype=torch.uint8, device="cuda")
+    t2 = dev(a)
+    with pytest.raises(ipls.IPLSError) as e:
+        ipls.sort(t2, k=1024, base_case=4096, key_type=0, workspace=small)
+    assert e.value.status == 4
+
+
+def test_deterministic_repeat(ipls):
+    a = datagen.generate("C5", 2_000_000)
+    t1, t2 = dev(a), dev(a)
+    r1 = ipls.sort_trace(t1, k=1024, base_case=4096, key_type=0)
+    r2 = ipls.sort_trace(t2, k=1024, base_case=4096, key_type=0)
+    assert torch.equal(t1, t2)
+    assert gpu_digests(r1.records) == gpu_digests(r2.records)
