@@ -1,0 +1,362 @@
+"""bench.py — IPLS distribution-step sort on B200: keys sorted/s and HBM roofline fraction.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE JSON line on
+rank 0.  A step is one whole sort (every level: sample, FMCD fit, classify+histogram,
+offsets, stable scatter; base case) of the BASELINE workload C2: n = 1e8 float64 keys
+i.i.d. Normal(0,1) (PCG64 seed 1), k = 1024 buckets per level, base case <= 4096 keys.
+
+* value     keys/s over all ranks, inputs resident in HBM when the timed region starts;
+            each step sorts a fresh copy of the pristine input (the restoring D2D copy is
+            outside the per-step CUDA-event window; the 0.8 GB input is > L2 (126 MB)).
+* e2e       the same metric through the C-ABI with HOST buffers (ipls_sort_host on pinned
+            memory): H2D copy + sort + D2H copy inside the timed region.
+* roofline  dominant kernel (largest share of the step), algorithmic bytes / CUDA-event
+            time measured by the library on its launching stream, vs MEASURED_PEAKS.json.
+* cpu_baseline  the CPU oracle (oracle/, single thread) on the same input, rank 0 only.
+* N > 1     replicas only: every rank sorts its own C2 instance; no
+            collective on the data path (the exchange-step design is future work).
+
+`--impl reference` times the oracle (the tier's reference arm) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "keys sorted/sec (float64, n=1e8, 1xB200)"
+UNIT = "keys/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+class ClockSampler:
+    """nvidia-smi style clock/throttle sampling DURING the timed region (NVML)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, nm in names.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(self.reasons),
+            "samples": len(self.samples),
+        }
+
+
+def dist_init(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64,
+                     device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_cpu_oracle(a: np.ndarray, cfg, max_keys: int):
+    """Time the CPU oracle (single thread) on a bounded prefix sample of the workload."""
+    import oracle
+    sample = np.ascontiguousarray(a[:max_keys]).copy()
+    t0 = time.perf_counter()
+    st = oracle.sort(sample, k=cfg.k, base_case=cfg.base_case).status
+    dt = time.perf_counter() - t0
+    assert st == 0
+    return sample.size / dt, dt, sample.size
+
+
+def bench_reference(args):
+    """--impl reference: the oracle as it stands on the host cores, per step a bounded
+    sample of the workload (rank 0 only under torchrun)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2208_06902_b200 import datagen
+    cfg = datagen.CONFIGS[args.config]
+    a = datagen.generate(args.config)
+    sample_n = args.ref_sample
+    rng = np.random.default_rng(0)
+    times = []
+    for step in range(args.warmup + args.steps):
+        off = int(rng.integers(0, a.size - sample_n + 1))
+        s = np.ascontiguousarray(a[off:off + sample_n]).copy()
+        import oracle
+        t0 = time.perf_counter()
+        assert oracle.sort(s, k=cfg.k, base_case=cfg.base_case).status == 0
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = sample_n * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg.desc}, n={cfg.n}, k={cfg.k}, "
+                               f"base_case={cfg.base_case}",
+                   "sample_keys_per_step": sample_n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{sample_n} contiguous keys of the {args.config} input per "
+                                   f"step (random offset), oracle single-threaded, "
+                                   f"host {cpu_model()} ({host_cores()} cores visible)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-sample", type=int, default=100_000_000,
+                    help="keys of the workload the CPU oracle sorts for cpu_baseline")
+    ap.add_argument("--ref-sample", type=int, default=2_000_000)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch of the dominant kernel (from profiles/)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        bench_reference(args)
+        return
+
+    import torch
+    import paper_2208_06902_b200 as ipls
+    from paper_2208_06902_b200 import datagen
+
+    world, rank, local = dist_init(args)
+    cfg = datagen.CONFIGS[args.config]
+    a = datagen.generate(args.config)
+    kt = ipls.KEY_F64 if a.dtype == np.float64 else ipls.KEY_U64
+    n = a.size
+    dev = torch.device("cuda", local)
+    pristine = torch.from_numpy(a.view(np.int64)).to(dev)
+    work = torch.empty_like(pristine)
+    st = torch.cuda.current_stream()
+
+    def one(timed_events=None):
+        work.copy_(pristine)
+        if timed_events is not None:
+            timed_events[0].record(st)
+        ipls.sort(work, k=cfg.k, base_case=cfg.base_case, key_type=kt)
+        if timed_events is not None:
+            timed_events[1].record(st)
+
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    # correctness of the timed configuration: sorted + same multiset as the input
+    chk = work.view(torch.float64) if kt == ipls.KEY_F64 else work
+    if kt == ipls.KEY_F64:
+        assert bool((chk[1:] >= chk[:-1]).all()), "output not sorted"
+    ref_sorted = torch.sort(pristine.view(torch.float64) if kt == ipls.KEY_F64 else pristine)[0]
+    assert torch.equal(ref_sorted.view(torch.int64), work), "output is not the sorted input"
+    del ref_sorted
+
+    sampler = ClockSampler(local)
+    ipls.profile_reset()
+    ipls.profile_enable(True)
+    launches0 = ipls.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    sampler.start()
+    for i in range(args.steps):
+        one(evs[i])
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = sampler.stop()
+    launches = ipls.launch_count() - launches0
+    ipls.profile_enable(False)
+    prof = ipls.profile_read()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    ms_local = sum(step_ms) / len(step_ms)
+    ms = allreduce_max(ms_local, world)
+    value = n * world / (ms / 1e3)
+
+    # roofline of the dominant kernel (largest share of the step)
+    peak, peak_kind = load_peaks()
+    tot_prof_ms = sum(v[1] for v in prof.values())
+    dom = max((k_ for k_ in prof if prof[k_][2] > 0), key=lambda k_: prof[k_][1])
+    d_launch, d_ms, d_bytes = prof[dom]
+    achieved = d_bytes / (d_ms / 1e3) / 1e9
+    shares = {k_: round(v[1] / tot_prof_ms, 4) for k_, v in sorted(prof.items())}
+    per_kernel = {k_: {"launches": v[0], "ms_per_step": round(v[1] / args.steps, 4),
+                       "alg_GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1) if v[2] > 0 else None}
+                  for k_, v in sorted(prof.items())}
+
+    # whole-sort roofline model: 2 * 8 B * n * (L* + 1)
+    import math
+    Lstar = math.ceil(math.log(math.ceil(n / cfg.base_case), cfg.k))
+    model_bytes = 2 * 8 * n * (Lstar + 1)
+    sort_frac_8tb = (model_bytes / 8e12) / (ms / 1e3)
+
+    # e2e: host buffers through the C-ABI (H2D + sort + D2H inside the timed region)
+    hbuf = torch.from_numpy(a.copy()).pin_memory()
+    hsrc = torch.from_numpy(a).pin_memory() if False else None  # noqa: F841
+    e2e_times = []
+    for i in range(args.e2e_steps + 1):
+        hbuf.numpy()[:] = a  # restore (outside the timed region)
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ipls.sort_host_ptr(hbuf.data_ptr(), n, kt, k=cfg.k, base_case=cfg.base_case)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if i > 0:
+            e2e_times.append(dt)
+    e2e_s = allreduce_max(statistics.median(e2e_times), world)
+    e2e_value = n * world / e2e_s
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        v, dt, ns = run_cpu_oracle(a, cfg, min(args.cpu_sample, n))
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {ns} keys of the {args.config} input ({dt:.1f} s, one run, "
+                         f"single thread; host {cpu_model()}, {host_cores()} cores visible)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if kt == ipls.KEY_F64 else "u64", "data": "synthetic",
+            "config": {
+                "workload": f"{args.config}: {cfg.desc}, n={n}, k={cfg.k}, base_case={cfg.base_case}",
+                "parallelism": "replicas" if world > 1 else "single-gpu",
+                "l2": "input 0.8 GB > L2 126 MB; pristine copy restored (D2D) before every step",
+                "timing": "CUDA events around each ipls_sort_ex call on its stream; mean over steps; max over ranks",
+                "sort_roofline_model": {"bytes_per_key": 16 * (Lstar + 1), "levels_L*": Lstar,
+                                        "frac_of_8TBps": round(sort_frac_8tb, 4),
+                                        "frac_of_measured_copy": round(
+                                            (model_bytes / (peak * 1e9)) / (ms / 1e3), 4)},
+                "kernel_shares": shares,
+                "per_kernel": per_kernel,
+                "workspace_bytes": ipls.workspace_bytes(n, kt, k=cfg.k, base_case=cfg.base_case),
+            },
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": args.traffic},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                    "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

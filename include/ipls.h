@@ -94,7 +94,7 @@ ipls_status ipls_sort_host(void* h_keys, size_t n, ipls_key_type t, const ipls_c
 
 /* FMCD fit (Listing 1, binary64, R3/R4) of one already-sorted sample.
  * d_sorted_sample: S keys of type t sorted by ordering key (device).  S >= 4, 3 <= k <=
- * IPLS_MAX_K, S <= 65536.  Writes *h_out.  Returns IPLS_ERR_DEGENERATE_SAMPLE (with
+ * IPLS_MAX_K, S <= 8192 (the fit kernel's smem sample).  Writes *h_out.  Returns IPLS_ERR_DEGENERATE_SAMPLE (with
  * h_out->kind = EQ3 and pivot_ok = ordering key of s[S/2]) when !(u_d > 0) or A, B are not
  * finite (R5). */
 ipls_status ipls_fit_fmcd(const void* d_sorted_sample, size_t S, ipls_key_type t, uint32_t k,
@@ -137,6 +137,22 @@ const char* ipls_status_string(ipls_status s);
 const char* ipls_last_cuda_error(void);
 /* Number of kernels the library enqueued since load (diagnostics / bench launch count). */
 uint64_t ipls_kernel_launch_count(void);
+
+/* ---- per-kernel timing (bench.py roofline) ----
+ * When enabled, every kernel launch is bracketed by CUDA events recorded on the launching
+ * stream; durations are collected when the call synchronises.  `bytes` is the launch's
+ * ALGORITHMIC traffic: 8 B/key read for classify, 16 B/key for scatter and
+ * base case, 8 B/key for fills; 0 for metadata kernels. */
+typedef struct {
+  char name[32];
+  uint64_t launches;
+  double total_ms;
+  double bytes;
+} ipls_profile_entry;
+void ipls_profile_enable(int on);
+void ipls_profile_reset(void);
+/* Copies up to cap entries into out; returns the number of distinct kernels. */
+size_t ipls_profile_read(ipls_profile_entry* out, size_t cap);
 
 #ifdef __cplusplus
 }

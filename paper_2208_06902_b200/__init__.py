@@ -71,11 +71,17 @@ class _Trace(ctypes.Structure):
                 ("levels", ctypes.c_uint32)]
 
 
+class _ProfEntry(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64),
+                ("total_ms", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
 # C-ABI symbols declared in include/ipls.h (tests check the .so exports all of them)
 SYMBOLS = ["ipls_default_config", "ipls_sort_f64", "ipls_sort_u64", "ipls_sort_ex",
            "ipls_workspace_bytes", "ipls_sort_host", "ipls_fit_fmcd", "ipls_partition_level",
            "ipls_sort_trace", "ipls_status_string", "ipls_last_cuda_error",
-           "ipls_kernel_launch_count"]
+           "ipls_kernel_launch_count", "ipls_profile_enable", "ipls_profile_reset",
+           "ipls_profile_read"]
 
 _lib = None
 
@@ -107,6 +113,10 @@ def lib():
         L.ipls_status_string.argtypes = [i32]; L.ipls_status_string.restype = ctypes.c_char_p
         L.ipls_last_cuda_error.restype = ctypes.c_char_p
         L.ipls_kernel_launch_count.restype = u64
+        L.ipls_profile_enable.argtypes = [i32]; L.ipls_profile_enable.restype = None
+        L.ipls_profile_reset.argtypes = []; L.ipls_profile_reset.restype = None
+        L.ipls_profile_read.argtypes = [ctypes.POINTER(_ProfEntry), sz]
+        L.ipls_profile_read.restype = sz
         _lib = L
     return _lib
 
@@ -143,6 +153,24 @@ def _key_type_of(t, key_type: Optional[int]) -> int:
 def _check_tensor(t):
     if not t.is_cuda or not t.is_contiguous() or t.element_size() != 8:
         raise ValueError("keys must be a contiguous CUDA tensor of 8-byte elements")
+
+
+def profile_enable(on: bool = True) -> None:
+    lib().ipls_profile_enable(1 if on else 0)
+
+
+def profile_reset() -> None:
+    lib().ipls_profile_reset()
+
+
+def profile_read() -> dict:
+    """{kernel: (launches, total_ms, algorithmic_bytes)} from the library's event timing."""
+    L = lib()
+    cnt = L.ipls_profile_read(None, 0)
+    arr = (_ProfEntry * max(1, cnt))()
+    L.ipls_profile_read(arr, cnt)
+    return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms),
+                                   float(arr[i].bytes)) for i in range(cnt)}
 
 
 def launch_count() -> int:

@@ -38,6 +38,72 @@ inline void ck_launch() {
   ck(cudaGetLastError());
 }
 
+// Optional per-kernel CUDA-event timing (ipls_profile_*): events bracket each launch on its
+// stream; durations are folded in when the call synchronises (prof_collect).
+struct ProfAcc {
+  uint64_t launches = 0;
+  double ms = 0.0, bytes = 0.0;
+};
+struct ProfPending {
+  const char* name;
+  double bytes;
+  cudaEvent_t e0, e1;
+};
+std::atomic<int> g_prof_on{0};
+std::mutex g_prof_mu;
+std::map<std::string, ProfAcc> g_prof;
+thread_local std::vector<ProfPending> t_pending;
+thread_local std::vector<cudaEvent_t> t_event_pool;
+
+cudaEvent_t prof_event() {
+  if (!t_event_pool.empty()) {
+    cudaEvent_t e = t_event_pool.back();
+    t_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  ck(cudaEventCreate(&e));
+  return e;
+}
+
+struct ProfScope {
+  bool on;
+  ProfPending p;
+  cudaStream_t st;
+  ProfScope(const char* name, double bytes, cudaStream_t s) : on(g_prof_on.load() != 0), st(s) {
+    if (on) {
+      p.name = name; p.bytes = bytes; p.e0 = prof_event(); p.e1 = prof_event();
+      ck(cudaEventRecord(p.e0, st));
+    }
+  }
+  ~ProfScope() {
+    if (on) {
+      cudaEventRecord(p.e1, st);
+      t_pending.push_back(p);
+    }
+  }
+};
+
+void prof_collect() {
+  if (t_pending.empty()) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& p : t_pending) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(p.e1) == cudaSuccess && cudaEventElapsedTime(&ms, p.e0, p.e1) == cudaSuccess) {
+      ProfAcc& a = g_prof[p.name];
+      a.launches += 1;
+      a.ms += ms;
+      a.bytes += p.bytes;
+    }
+    t_event_pool.push_back(p.e0);
+    t_event_pool.push_back(p.e1);
+  }
+  t_pending.clear();
+}
+#define IPLS_CAT2(a, b) a##b
+#define IPLS_CAT(a, b) IPLS_CAT2(a, b)
+#define IPLS_PROF(name, bytes) ProfScope IPLS_CAT(_prof_scope_, __LINE__)(name, (double)(bytes), st)
+
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Params {
@@ -246,8 +312,11 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     Window w{0, (uint32_t)n, 0};
     Window* dw = at<Window>(fixed, FL.wins[0]);
     ck(cudaMemcpyAsync(dw, &w, sizeof(Window), cudaMemcpyHostToDevice, st));
-    k_base_sort<F64><<<1, kBaseThreads, base_smem(), st>>>(dw, keys, scr, d_err, F64 ? 1 : 0);
-    ck_launch();
+    {
+      IPLS_PROF("base_sort", 16.0 * n);
+      k_base_sort<F64><<<1, kBaseThreads, base_smem(), st>>>(dw, keys, scr, d_err, F64 ? 1 : 0);
+      ck_launch();
+    }
     uint32_t herr = 0;
     ck(cudaMemcpyAsync(&h_ctr[1].err, d_err, 4, cudaMemcpyDeviceToHost, st));
     ck(cudaStreamSynchronize(st));
@@ -261,6 +330,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
   uint32_t nchunk = (uint32_t)((n + p.chunk_keys - 1) / p.chunk_keys);
   uint32_t nunit = (nchunk + kUnitChunks - 1) / kUnitChunks;
   uint32_t nsample = sample_size(n, k);
+  uint64_t level_keys = n;
   k_init_root<<<std::max<uint32_t>(1, (nchunk + 255) / 256), 256, 0, st>>>(
       at<SegDesc>(fixed, FL.segs[0]), at<ChunkDesc>(fixed, FL.chunks[0]),
       at<UnitDesc>(fixed, FL.units[0]), n, nsample, p.chunk_keys, 0u);
@@ -296,20 +366,35 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     uint64_t* seg_dst = at<uint64_t>(meta, ML.seg_dst);
 
     ck(cudaMemsetAsync(nctr, 0, sizeof(LevelCounters), st));
-    k_sample_gather<F64><<<nseg, 256, 0, st>>>(src, segs, seed, level, samples);
-    ck_launch();
-    k_fit<F64><<<nseg, kFitThreads, fit_smem(), st>>>(segs, samples, k, models, 0);
-    ck_launch();
-    k_classify_hist<F64><<<nchunk, kTileThreads, classify_smem(k), st>>>(
-        src, chunks, segs, models, k, chunk_hist, chunk_rep, d_err,
-        (F64 && level == 0) ? 1 : 0, nullptr, 0);
-    ck_launch();
-    k_unit_reduce<<<col_blocks(nunit, k), 256, 0, st>>>(units, nunit, k, chunk_hist, chunk_rep,
-                                                         unit_cnt, unit_rep);
-    ck_launch();
-    k_seg_scan<<<col_blocks(nseg, k), 256, 0, st>>>(segs, nseg, k, unit_cnt, unit_rep, seg_tot,
-                                                     seg_rep);
-    ck_launch();
+    {
+      IPLS_PROF("sample_gather", 0);
+      k_sample_gather<F64><<<nseg, 256, 0, st>>>(src, segs, seed, level, samples);
+      ck_launch();
+    }
+    {
+      IPLS_PROF("fit", 0);
+      k_fit<F64><<<nseg, kFitThreads, fit_smem(), st>>>(segs, samples, k, models, 0);
+      ck_launch();
+    }
+    {
+      IPLS_PROF("classify_hist", 8.0 * level_keys);
+      k_classify_hist<F64><<<nchunk, kTileThreads, classify_smem(k), st>>>(
+          src, chunks, segs, models, k, chunk_hist, chunk_rep, d_err,
+          (F64 && level == 0) ? 1 : 0, nullptr, 0);
+      ck_launch();
+    }
+    {
+      IPLS_PROF("unit_reduce", 0);
+      k_unit_reduce<<<col_blocks(nunit, k), 256, 0, st>>>(units, nunit, k, chunk_hist,
+                                                           chunk_rep, unit_cnt, unit_rep);
+      ck_launch();
+    }
+    {
+      IPLS_PROF("seg_scan", 0);
+      k_seg_scan<<<col_blocks(nseg, k), 256, 0, st>>>(segs, nseg, k, unit_cnt, unit_rep,
+                                                       seg_tot, seg_rep);
+      ck_launch();
+    }
     OffsetsArgs oa;
     oa.segs = segs; oa.models = models; oa.seg_tot = seg_tot; oa.seg_rep = seg_rep;
     oa.seg_dst = seg_dst; oa.k = k; oa.base_case = p.B; oa.level = level;
@@ -322,12 +407,22 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     oa.cap_samples = p.cap_samples;
     oa.wins = wins; oa.cap_wins = p.cap_wins; oa.fills = fills; oa.cap_fills = p.cap_fills;
     oa.err = d_err;
-    k_seg_offsets<<<nseg, kOffThreads, 0, st>>>(oa);
-    ck_launch();
-    k_chunk_prefix<<<col_blocks(nunit, k), 256, 0, st>>>(units, nunit, k, unit_cnt, chunk_hist);
-    ck_launch();
-    launch_scatter<F64>(p.log2k, dim3(nchunk), scatter_smem(k), st, src, keys, scr, chunks,
-                        models, k, chunk_hist, seg_dst, d_err);
+    {
+      IPLS_PROF("seg_offsets", 0);
+      k_seg_offsets<<<nseg, kOffThreads, 0, st>>>(oa);
+      ck_launch();
+    }
+    {
+      IPLS_PROF("chunk_prefix", 0);
+      k_chunk_prefix<<<col_blocks(nunit, k), 256, 0, st>>>(units, nunit, k, unit_cnt,
+                                                            chunk_hist);
+      ck_launch();
+    }
+    {
+      IPLS_PROF("scatter", 16.0 * level_keys);
+      launch_scatter<F64>(p.log2k, dim3(nchunk), scatter_smem(k), st, src, keys, scr, chunks,
+                          models, k, chunk_hist, seg_dst, d_err);
+    }
 
     if (trace) {
       std::vector<SegDesc> hs(nseg);
@@ -376,20 +471,24 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
 
     // base case of this level's base children, fills of its homogeneous children
     if (c.n_windows) {
+      IPLS_PROF("base_sort", 16.0 * c.win_keys);
       k_base_sort<F64><<<c.n_windows, kBaseThreads, base_smem(), st>>>(wins, keys, scr, d_err, 0);
       ck_launch();
     }
     if (c.n_fills) {
+      IPLS_PROF("fill", 8.0 * c.fill_keys);
       k_fill<<<c.n_fills, 256, 0, st>>>(fills, keys);
       ck_launch();
     }
     if (trace) trace->tr->levels = level + 1;
     nseg = c.n_segs;
+    level_keys = c.keys;
     nchunk = c.n_chunks;
     nunit = c.n_units;
     nsample = c.n_samples;
   }
   ck(cudaStreamSynchronize(st));
+  prof_collect();
   return IPLS_OK;
 }
 
@@ -438,6 +537,7 @@ ipls_status sort_impl(void* d_keys, size_t n, ipls_key_type t, const ipls_config
                              meta_cache, sc.h_ctr, st, cfg.seed, tr ? &sink : nullptr)
             : run_sort<false>(static_cast<uint64_t*>(d_keys), p, fixed, meta_in, meta_bytes,
                               meta_cache, sc.h_ctr, st, cfg.seed, tr ? &sink : nullptr);
+    prof_collect();
     if (tr) {
       // order records by (level, begin)
       std::vector<size_t> idx(sink.recs.size());
@@ -673,5 +773,29 @@ const char* ipls_status_string(ipls_status s) {
 const char* ipls_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
 
 uint64_t ipls_kernel_launch_count(void) { return g_launches.load(); }
+
+void ipls_profile_enable(int on) { g_prof_on.store(on ? 1 : 0); }
+
+void ipls_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.clear();
+}
+
+size_t ipls_profile_read(ipls_profile_entry* out, size_t cap) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  size_t i = 0;
+  for (auto& kv : g_prof) {
+    if (out && i < cap) {
+      ipls_profile_entry& e = out[i];
+      std::memset(&e, 0, sizeof(e));
+      std::strncpy(e.name, kv.first.c_str(), sizeof(e.name) - 1);
+      e.launches = kv.second.launches;
+      e.total_ms = kv.second.ms;
+      e.bytes = kv.second.bytes;
+    }
+    ++i;
+  }
+  return i;
+}
 
 }  // extern "C"

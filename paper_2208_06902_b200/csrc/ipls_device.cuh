@@ -59,6 +59,8 @@ struct LevelCounters {      // device-side counters of the level being built
   uint32_t n_segs, n_chunks, n_units, n_samples;
   uint32_t n_windows, n_fills, err, pad;
   uint64_t keys;            // keys in next-level segments
+  uint64_t win_keys;        // keys in this level's base-case windows
+  uint64_t fill_keys;       // keys in this level's fills
 };
 
 constexpr uint32_t kErrNan = 1u;

@@ -473,6 +473,7 @@ __global__ __launch_bounds__(kOffThreads) void k_seg_offsets(OffsetsArgs a) {
       wv.len = s_wend[widx] - s_wbeg[widx];
       wv.buf = dstbuf;
       a.wins[gi] = wv;
+      atomicAdd((unsigned long long*)&a.nctr->win_keys, (unsigned long long)wv.len);
     } else {
       atomicOr(a.err, kErrOverflow);
     }
@@ -489,6 +490,7 @@ __global__ __launch_bounds__(kOffThreads) void k_seg_offsets(OffsetsArgs a) {
       Fill f;
       f.begin = sg.begin + base; f.len = tot; f.value = a.seg_rep[(size_t)s * k + b]; f.pad = 0;
       a.fills[gi] = f;
+      atomicAdd((unsigned long long*)&a.nctr->fill_keys, (unsigned long long)tot);
     } else {
       atomicOr(a.err, kErrOverflow);
     }
