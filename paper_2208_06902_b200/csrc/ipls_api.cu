@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -108,15 +109,15 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Params {
   uint64_t n;
-  uint32_t k, B, chunk_keys, log2k;
-  uint32_t cap_segs, cap_chunks, cap_units, cap_samples, cap_wins, cap_fills;
+  uint32_t k, B, chunk_keys;
+  uint32_t cap_segs, cap_chunks, cap_samples, cap_wins, cap_fills;
 };
 
 uint32_t pick_chunk_keys(uint64_t n) {
-  // ~4 waves of 2 CTAs per SM over 148 SMs at level 0, whole tiles, 4096..65536 keys.
+  // ~8 chunks per SM at level 0 (148 SMs), whole tiles, 4096..65536 keys.
   uint64_t c = n / (148 * 8);
-  c = (c + kTile - 1) / kTile * kTile;
-  if (c < (uint64_t)kTile) c = kTile;
+  c = (c + kCTile - 1) / kCTile * kCTile;
+  if (c < (uint64_t)kCTile) c = kCTile;
   if (c > 65536) c = 65536;
   return (uint32_t)c;
 }
@@ -125,18 +126,14 @@ Params make_params(uint64_t n, uint32_t k, uint32_t B) {
   Params p{};
   p.n = n; p.k = k; p.B = B;
   p.chunk_keys = pick_chunk_keys(n);
-  p.log2k = 0;
-  while ((1u << p.log2k) < k) ++p.log2k;
   const uint64_t segs = n / ((uint64_t)B + 1) + 2;
   const uint64_t chunks = n / p.chunk_keys + segs + 1;
-  const uint64_t units = chunks / kUnitChunks + segs + 1;
   const uint64_t smax = sample_size(n, k);
   uint64_t samples = std::min<uint64_t>(n / 2 + 8, segs * smax + 8);
   uint64_t wins = std::min<uint64_t>(n + 1, n / ((uint64_t)B + 1) + n / kWindowNominal + 2 * segs) + 16;
   uint64_t fills = n / ((uint64_t)B + 1) + 16;
   p.cap_segs = (uint32_t)segs;
   p.cap_chunks = (uint32_t)chunks;
-  p.cap_units = (uint32_t)units;
   p.cap_samples = (uint32_t)samples;
   p.cap_wins = (uint32_t)wins;
   p.cap_fills = (uint32_t)fills;
@@ -146,7 +143,7 @@ Params make_params(uint64_t n, uint32_t k, uint32_t B) {
 // Fixed part of the workspace: scratch keys + descriptors of two levels + windows/fills of
 // two levels + counters.  The k-scaled per-level metadata is carved after it.
 struct FixedLayout {
-  size_t scratch, segs[2], chunks[2], units[2], wins[2], fills[2], ctr[2], err, total;
+  size_t scratch, segs[2], chunks[2], wins[2], fills[2], ctr[2], err, total;
 };
 
 FixedLayout fixed_layout(const Params& p) {
@@ -157,7 +154,6 @@ FixedLayout fixed_layout(const Params& p) {
   for (int i = 0; i < 2; ++i) {
     L.segs[i] = take((size_t)p.cap_segs * sizeof(SegDesc));
     L.chunks[i] = take((size_t)p.cap_chunks * sizeof(ChunkDesc));
-    L.units[i] = take((size_t)p.cap_units * sizeof(UnitDesc));
     L.wins[i] = take((size_t)p.cap_wins * sizeof(Window));
     L.fills[i] = take((size_t)p.cap_fills * sizeof(Fill));
     L.ctr[i] = take(sizeof(LevelCounters));
@@ -167,37 +163,37 @@ FixedLayout fixed_layout(const Params& p) {
   return L;
 }
 
+// Per-level metadata (sized by the level's actual counts).  `status` comes first so a fresh
+// allocation can be cleared cheaply.
 struct MetaLayout {
-  size_t models, samples, chunk_hist, chunk_rep, unit_cnt, unit_rep, seg_tot, seg_rep, seg_dst,
-      total;
+  size_t status, cnt_agg, rep_agg, chunk_pre, models, samples, seg_dst, seg_tot, total;
 };
 
-MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t units, uint64_t samples,
-                       uint32_t k) {
+MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_t k) {
   MetaLayout L{};
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+  L.status = take(chunks * k * 8);
+  L.cnt_agg = take(chunks * k * 4);
+  L.rep_agg = take(chunks * k * 8);
+  L.chunk_pre = take(chunks * k * 4);
   L.models = take(segs * sizeof(ModelDev));
   L.samples = take(samples * 8 + 64);
-  L.chunk_hist = take(chunks * k * 4);
-  L.chunk_rep = take(chunks * k * 8);
-  L.unit_cnt = take(units * k * 4);
-  L.unit_rep = take(units * k * 8);
-  L.seg_tot = take(segs * k * 4);
-  L.seg_rep = take(segs * k * 8);
   L.seg_dst = take(segs * k * 8);
+  L.seg_tot = take(segs * k * 4);
   L.total = o;
   return L;
 }
 
 size_t worst_meta_bytes(const Params& p) {
-  return meta_layout(p.cap_segs, p.cap_chunks, p.cap_units, p.cap_samples, p.k).total;
+  return meta_layout(p.cap_segs, p.cap_chunks, p.cap_samples, p.k).total;
 }
 
 // Device buffers for one call: either the caller's workspace or the per-stream cache.
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
+  bool fresh = false;  // set when (re)allocated: lookback status words must be cleared
   void release() {
     if (ptr) cudaFree(ptr);
     ptr = nullptr;
@@ -208,11 +204,12 @@ struct DevBuf {
     release();
     ck(cudaMalloc(&ptr, want));
     bytes = want;
+    fresh = true;
   }
 };
 
 struct StreamCache {
-  DevBuf fixed, meta, io;  // io: device copy for ipls_sort_host
+  DevBuf fixed, meta, io;          // io: device copy for ipls_sort_host
   LevelCounters* h_ctr = nullptr;  // pinned
   StreamCache() { ck(cudaMallocHost((void**)&h_ctr, 2 * sizeof(LevelCounters) + 64)); }
   ~StreamCache() {
@@ -223,6 +220,7 @@ struct StreamCache {
 
 std::mutex g_mu;
 std::map<std::pair<int, void*>, std::unique_ptr<StreamCache>> g_cache;
+std::atomic<uint32_t> g_epoch{0};
 
 StreamCache& cache_for(void* stream) {
   int dev = 0;
@@ -248,50 +246,48 @@ struct TraceSink {
   std::vector<std::vector<uint64_t>> counts, samples;
 };
 
-template <bool F64>
-void launch_scatter(uint32_t log2k, dim3 grid, size_t smem, cudaStream_t st,
-                    const uint64_t* src, uint64_t* user, uint64_t* scr, const ChunkDesc* chunks,
-                    const ModelDev* models, uint32_t k, const uint32_t* chunk_pre,
-                    const uint64_t* seg_dst, const uint32_t* err) {
-#define IPLS_SC(L)                                                                          \
-  case L:                                                                                   \
-    ck(cudaFuncSetAttribute(k_scatter<F64, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                            (int)smem));                                                    \
-    k_scatter<F64, L><<<grid, kTileThreads, smem, st>>>(src, user, scr, chunks, models, k,  \
-                                                       chunk_pre, seg_dst, err);            \
-    break;
-  switch (log2k) {
-    IPLS_SC(2) IPLS_SC(3) IPLS_SC(4) IPLS_SC(5) IPLS_SC(6) IPLS_SC(7) IPLS_SC(8) IPLS_SC(9)
-    IPLS_SC(10)
-    default: throw CudaFail{cudaErrorInvalidValue};
-  }
-#undef IPLS_SC
-  ck_launch();
-}
-
 size_t scatter_smem(uint32_t k) {
-  return (size_t)kTile * 8 + (size_t)k * 8 + (size_t)k * 8 + (size_t)kTileWarps * k * 2 +
-         (size_t)kTile * 2;
+  return (size_t)kSTile * 8 + (size_t)k * 8 + (size_t)k * kPendSlots * 8 + (size_t)kSTile * 4 +
+         (size_t)(kSWarps / 2) * k * 4 + (size_t)(k + 1) * 4 + (size_t)k * 8 + (size_t)k;
+}
+template <bool F64>
+void launch_scatter(uint32_t nchunk, cudaStream_t st, const uint64_t* src, uint64_t* user,
+                    uint64_t* scr, const ChunkDesc* chunks, const ModelDev* models, uint32_t k,
+                    const uint32_t* chunk_pre, const uint64_t* seg_dst, const uint32_t* err) {
+  k_scatter<F64><<<nchunk, kSThreads, scatter_smem(k), st>>>(src, user, scr, chunks, models, k,
+                                                             chunk_pre, seg_dst, err);
+  ck_launch();
 }
 size_t classify_smem(uint32_t k) { return (size_t)k * 8 + (size_t)k * 12; }
 size_t base_smem() { return (size_t)kBaseMax * 12; }
-size_t fit_smem() { return (size_t)kFitMaxS * 8; }
+uint32_t fit_cap(uint32_t maxS) {
+  uint32_t c = 64;
+  while (c < maxS) c <<= 1;
+  return c;
+}
+size_t fit_smem(uint32_t cap) { return (size_t)cap * 20; }
 
 template <bool F64>
 void set_attrs() {
   static bool done = false;
   if (done) return;
-  ck(cudaFuncSetAttribute(k_fit<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fit_smem()));
+  ck(cudaFuncSetAttribute(k_gather_fit<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)fit_smem(kFitMaxS)));
   ck(cudaFuncSetAttribute(k_base_sort<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)base_smem()));
-  ck(cudaFuncSetAttribute(k_classify_hist<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ck(cudaFuncSetAttribute(k_classify_scan<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)classify_smem(kMaxK)));
+  ck(cudaFuncSetAttribute(k_scatter<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)scatter_smem(kMaxK)));
+
   done = true;
 }
 
-uint32_t col_blocks(uint64_t items, uint32_t k) {
-  uint64_t warps = items * ((k + 31) / 32);
-  return (uint32_t)std::max<uint64_t>(1, (warps + 7) / 8);
+uint32_t next_epoch(bool* wrapped) {
+  uint32_t e = g_epoch.fetch_add(1) + 1;
+  *wrapped = (e & 0xffff) == 0;
+  if (*wrapped) e = g_epoch.fetch_add(1) + 1;
+  return e & 0xffff;
 }
 
 // Run the whole level-batched sort.  keys: device array (user buffer).
@@ -317,23 +313,22 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
       k_base_sort<F64><<<1, kBaseThreads, base_smem(), st>>>(dw, keys, scr, d_err, F64 ? 1 : 0);
       ck_launch();
     }
-    uint32_t herr = 0;
     ck(cudaMemcpyAsync(&h_ctr[1].err, d_err, 4, cudaMemcpyDeviceToHost, st));
     ck(cudaStreamSynchronize(st));
-    herr = h_ctr[1].err;
-    if (herr & kErrNan) return IPLS_ERR_NAN_KEY;
+    if (h_ctr[1].err & kErrNan) return IPLS_ERR_NAN_KEY;
     return IPLS_OK;
   }
 
   // level-0 work: the root segment
   uint32_t nseg = 1;
   uint32_t nchunk = (uint32_t)((n + p.chunk_keys - 1) / p.chunk_keys);
-  uint32_t nunit = (nchunk + kUnitChunks - 1) / kUnitChunks;
   uint32_t nsample = sample_size(n, k);
+  uint32_t max_S = nsample;
   uint64_t level_keys = n;
+  ck(cudaMemsetAsync(at<LevelCounters>(fixed, FL.ctr[0]), 0, sizeof(LevelCounters), st));
   k_init_root<<<std::max<uint32_t>(1, (nchunk + 255) / 256), 256, 0, st>>>(
-      at<SegDesc>(fixed, FL.segs[0]), at<ChunkDesc>(fixed, FL.chunks[0]),
-      at<UnitDesc>(fixed, FL.units[0]), n, nsample, p.chunk_keys, 0u);
+      at<SegDesc>(fixed, FL.segs[0]), at<ChunkDesc>(fixed, FL.chunks[0]), n, nsample,
+      p.chunk_keys, 0u);
   ck_launch();
 
   for (uint32_t level = 0; nseg > 0; ++level) {
@@ -341,87 +336,73 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     const uint64_t* src = (cur == 0) ? keys : scr;
     SegDesc* segs = at<SegDesc>(fixed, FL.segs[cur]);
     ChunkDesc* chunks = at<ChunkDesc>(fixed, FL.chunks[cur]);
-    UnitDesc* units = at<UnitDesc>(fixed, FL.units[cur]);
+    LevelCounters* cctr = at<LevelCounters>(fixed, FL.ctr[cur]);
     LevelCounters* nctr = at<LevelCounters>(fixed, FL.ctr[nxt]);
     Window* wins = at<Window>(fixed, FL.wins[cur]);
     Fill* fills = at<Fill>(fixed, FL.fills[cur]);
 
     // per-level metadata, sized by this level's actual counts
-    MetaLayout ML = meta_layout(nseg, nchunk, nunit, nsample, k);
+    const MetaLayout ML = meta_layout(nseg, nchunk, nsample, k);
     void* meta = d_meta_in;
+    bool clear_status = false;
     if (meta_cache) {
       meta_cache->ensure(ML.total);
       meta = meta_cache->ptr;
-    } else if (ML.total > meta_bytes_in) {
-      return IPLS_ERR_OUT_OF_MEMORY;
+      if (meta_cache->fresh) {
+        ck(cudaMemsetAsync(meta, 0, meta_cache->bytes, st));
+        meta_cache->fresh = false;
+      }
+    } else {
+      if (ML.total > meta_bytes_in) return IPLS_ERR_OUT_OF_MEMORY;
+      clear_status = true;  // caller memory: no history of epochs
     }
+    bool wrapped = false;
+    const uint32_t epoch = next_epoch(&wrapped);
+    if (clear_status || wrapped)
+      ck(cudaMemsetAsync(at<uint64_t>(meta, ML.status), 0, (size_t)nchunk * k * 8, st));
     ModelDev* models = at<ModelDev>(meta, ML.models);
     uint64_t* samples = at<uint64_t>(meta, ML.samples);
-    uint32_t* chunk_hist = at<uint32_t>(meta, ML.chunk_hist);
-    uint64_t* chunk_rep = at<uint64_t>(meta, ML.chunk_rep);
-    uint32_t* unit_cnt = at<uint32_t>(meta, ML.unit_cnt);
-    uint64_t* unit_rep = at<uint64_t>(meta, ML.unit_rep);
-    uint32_t* seg_tot = at<uint32_t>(meta, ML.seg_tot);
-    uint64_t* seg_rep = at<uint64_t>(meta, ML.seg_rep);
     uint64_t* seg_dst = at<uint64_t>(meta, ML.seg_dst);
+    uint32_t* seg_tot = at<uint32_t>(meta, ML.seg_tot);
+    uint32_t* chunk_pre = at<uint32_t>(meta, ML.chunk_pre);
 
     ck(cudaMemsetAsync(nctr, 0, sizeof(LevelCounters), st));
     {
-      IPLS_PROF("sample_gather", 0);
-      k_sample_gather<F64><<<nseg, 256, 0, st>>>(src, segs, seed, level, samples);
+      IPLS_PROF("gather_fit", 0);
+      const uint32_t cap = fit_cap(max_S);
+      k_gather_fit<F64><<<nseg, kFitThreads, fit_smem(cap), st>>>(
+          src, segs, seed, level, k, cap, trace ? samples : nullptr, models, nullptr);
       ck_launch();
     }
+    LevelArgs la{};
+    la.src = src; la.segs = segs; la.chunks = chunks; la.models = models;
+    la.k = k; la.base_case = p.B; la.level = level; la.chunk_keys = p.chunk_keys;
+    la.ticket = &cctr->ticket;
+    la.status = at<uint64_t>(meta, ML.status);
+    la.cnt_agg = at<uint32_t>(meta, ML.cnt_agg);
+    la.rep_agg = at<uint64_t>(meta, ML.rep_agg);
+    la.chunk_pre = chunk_pre;
+    la.seg_dst = seg_dst;
+    la.seg_tot = trace ? seg_tot : nullptr;
+    la.epoch = epoch;
+    la.err = d_err;
+    la.check_nan = (F64 && level == 0) ? 1 : 0;
+    la.ids = nullptr;
+    la.single_offsets = nullptr;
+    la.nsegs = at<SegDesc>(fixed, FL.segs[nxt]);
+    la.nchunks = at<ChunkDesc>(fixed, FL.chunks[nxt]);
+    la.nctr = nctr;
+    la.cap_segs = p.cap_segs; la.cap_chunks = p.cap_chunks; la.cap_samples = p.cap_samples;
+    la.wins = wins; la.cap_wins = p.cap_wins; la.fills = fills; la.cap_fills = p.cap_fills;
     {
-      IPLS_PROF("fit", 0);
-      k_fit<F64><<<nseg, kFitThreads, fit_smem(), st>>>(segs, samples, k, models, 0);
-      ck_launch();
-    }
-    {
-      IPLS_PROF("classify_hist", 8.0 * level_keys);
-      k_classify_hist<F64><<<nchunk, kTileThreads, classify_smem(k), st>>>(
-          src, chunks, segs, models, k, chunk_hist, chunk_rep, d_err,
-          (F64 && level == 0) ? 1 : 0, nullptr, 0);
-      ck_launch();
-    }
-    {
-      IPLS_PROF("unit_reduce", 0);
-      k_unit_reduce<<<col_blocks(nunit, k), 256, 0, st>>>(units, nunit, k, chunk_hist,
-                                                           chunk_rep, unit_cnt, unit_rep);
-      ck_launch();
-    }
-    {
-      IPLS_PROF("seg_scan", 0);
-      k_seg_scan<<<col_blocks(nseg, k), 256, 0, st>>>(segs, nseg, k, unit_cnt, unit_rep,
-                                                       seg_tot, seg_rep);
-      ck_launch();
-    }
-    OffsetsArgs oa;
-    oa.segs = segs; oa.models = models; oa.seg_tot = seg_tot; oa.seg_rep = seg_rep;
-    oa.seg_dst = seg_dst; oa.k = k; oa.base_case = p.B; oa.level = level;
-    oa.chunk_keys = p.chunk_keys;
-    oa.nsegs = at<SegDesc>(fixed, FL.segs[nxt]);
-    oa.nchunks = at<ChunkDesc>(fixed, FL.chunks[nxt]);
-    oa.nunits = at<UnitDesc>(fixed, FL.units[nxt]);
-    oa.nctr = nctr;
-    oa.cap_segs = p.cap_segs; oa.cap_chunks = p.cap_chunks; oa.cap_units = p.cap_units;
-    oa.cap_samples = p.cap_samples;
-    oa.wins = wins; oa.cap_wins = p.cap_wins; oa.fills = fills; oa.cap_fills = p.cap_fills;
-    oa.err = d_err;
-    {
-      IPLS_PROF("seg_offsets", 0);
-      k_seg_offsets<<<nseg, kOffThreads, 0, st>>>(oa);
-      ck_launch();
-    }
-    {
-      IPLS_PROF("chunk_prefix", 0);
-      k_chunk_prefix<<<col_blocks(nunit, k), 256, 0, st>>>(units, nunit, k, unit_cnt,
-                                                            chunk_hist);
+      IPLS_PROF("classify_scan", 8.0 * level_keys);
+      k_classify_scan<F64><<<nchunk, kCThreads, classify_smem(k), st>>>(la);
       ck_launch();
     }
     {
       IPLS_PROF("scatter", 16.0 * level_keys);
-      launch_scatter<F64>(p.log2k, dim3(nchunk), scatter_smem(k), st, src, keys, scr, chunks,
-                          models, k, chunk_hist, seg_dst, d_err);
+      launch_scatter<F64>(nchunk, st, src, keys, scr, chunks, models, k, chunk_pre, seg_dst,
+                          d_err);
     }
 
     if (trace) {
@@ -432,7 +413,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
       ck(cudaMemcpyAsync(hs.data(), segs, nseg * sizeof(SegDesc), cudaMemcpyDeviceToHost, st));
       ck(cudaMemcpyAsync(hm.data(), models, nseg * sizeof(ModelDev), cudaMemcpyDeviceToHost, st));
       ck(cudaMemcpyAsync(ht.data(), seg_tot, ht.size() * 4, cudaMemcpyDeviceToHost, st));
-      ck(cudaMemcpyAsync(hsmp.data(), samples, nsample * 8, cudaMemcpyDeviceToHost, st));
+      ck(cudaMemcpyAsync(hsmp.data(), samples, (size_t)nsample * 8, cudaMemcpyDeviceToHost, st));
       if (trace->tr->d_snapshots && level < trace->tr->snapshot_levels) {
         uint64_t* snap = static_cast<uint64_t*>(trace->tr->d_snapshots) + (size_t)level * n;
         if (level > 0)
@@ -449,7 +430,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
         std::vector<uint64_t> c(r.k_eff);
         r.requeued = 0;
         for (uint32_t b = 0; b < r.k_eff; ++b) {
-          c[b] = ht[(size_t)s * k + b] & ~kInhBit;
+          c[b] = ht[(size_t)s * k + b];
           if (hm[s].kind == kModelLinear && c[b] == hs[s].m) r.requeued = 1;
         }
         std::vector<uint64_t> smp(hsmp.begin() + hs[s].sample_off,
@@ -484,11 +465,10 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     nseg = c.n_segs;
     level_keys = c.keys;
     nchunk = c.n_chunks;
-    nunit = c.n_units;
     nsample = c.n_samples;
+    max_S = c.max_S;
   }
   ck(cudaStreamSynchronize(st));
-  prof_collect();
   return IPLS_OK;
 }
 
@@ -565,6 +545,7 @@ ipls_status sort_impl(void* d_keys, size_t n, ipls_key_type t, const ipls_config
     }
     return r;
   } catch (const CudaFail& f) {
+    prof_collect();
     g_last_cuda_error = cudaGetErrorString(f.e);
     return f.e == cudaErrorMemoryAllocation ? IPLS_ERR_OUT_OF_MEMORY : IPLS_ERR_CUDA;
   }
@@ -640,25 +621,26 @@ ipls_status ipls_fit_fmcd(const void* d_sorted_sample, size_t S, ipls_key_type t
     StreamCache& sc = cache_for(stream);
     const size_t need = align_up(S * 8, 256) + 256 + 256;
     sc.meta.ensure(need);
+    sc.meta.fresh = true;  // the lookback region is clobbered; clear it before the next sort
     uint64_t* smp = static_cast<uint64_t*>(sc.meta.ptr);
     SegDesc* dseg = at<SegDesc>(sc.meta.ptr, align_up(S * 8, 256));
     ModelDev* dmod = at<ModelDev>(sc.meta.ptr, align_up(S * 8, 256) + 256);
-    if (t == IPLS_KEY_F64) {
-      set_attrs<true>();
-      k_keys_to_ok_f64<<<(uint32_t)((S + 255) / 256), 256, 0, st>>>(
-          static_cast<const uint64_t*>(d_sorted_sample), smp, (uint32_t)S);
-      ck_launch();
-    } else {
-      set_attrs<false>();
-      ck(cudaMemcpyAsync(smp, d_sorted_sample, S * 8, cudaMemcpyDeviceToDevice, st));
-    }
+    k_keys_to_ok<<<(uint32_t)((S + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint64_t*>(d_sorted_sample), smp, (uint32_t)S, t == IPLS_KEY_F64);
+    ck_launch();
     SegDesc sd{};
     sd.S = (uint32_t)S;
     ck(cudaMemcpyAsync(dseg, &sd, sizeof(sd), cudaMemcpyHostToDevice, st));
-    if (t == IPLS_KEY_F64)
-      k_fit<true><<<1, kFitThreads, fit_smem(), st>>>(dseg, smp, k, dmod, 1);
-    else
-      k_fit<false><<<1, kFitThreads, fit_smem(), st>>>(dseg, smp, k, dmod, 1);
+    const uint32_t cap = fit_cap((uint32_t)S);
+    if (t == IPLS_KEY_F64) {
+      set_attrs<true>();
+      k_gather_fit<true><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, k, cap,
+                                                                nullptr, dmod, smp);
+    } else {
+      set_attrs<false>();
+      k_gather_fit<false><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, k, cap,
+                                                                 nullptr, dmod, smp);
+    }
     ck_launch();
     ModelDev hm;
     ck(cudaMemcpyAsync(&hm, dmod, sizeof(hm), cudaMemcpyDeviceToHost, st));
@@ -683,11 +665,10 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
   if (!eq3 && h_model->kind != IPLS_MODEL_LINEAR) return IPLS_ERR_INVALID_ARGUMENT;
   const uint32_t k = eq3 ? 3u : h_model->k;
   if (k < 3 || k > IPLS_MAX_K) return IPLS_ERR_INVALID_ARGUMENT;
-  const uint32_t k_eff = k;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   try {
     if (n == 0) {
-      std::vector<uint64_t> z(k_eff + 1, 0);
+      std::vector<uint64_t> z(k + 1, 0);
       ck(cudaMemcpyAsync(d_offsets, z.data(), z.size() * 8, cudaMemcpyHostToDevice, st));
       ck(cudaStreamSynchronize(st));
       return IPLS_OK;
@@ -695,58 +676,54 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
     StreamCache& sc = cache_for(stream);
     const uint32_t ck_keys = pick_chunk_keys(n);
     const uint32_t nchunk = (uint32_t)((n + ck_keys - 1) / ck_keys);
-    const uint32_t nunit = (nchunk + kUnitChunks - 1) / kUnitChunks;
-    MetaLayout ML = meta_layout(1, nchunk, nunit, 0, k);
+    const MetaLayout ML = meta_layout(1, nchunk, 0, k);
     size_t o = align_up(ML.total, 256);
     const size_t off_seg = o; o += 256;
     const size_t off_ch = o; o = align_up(o + nchunk * sizeof(ChunkDesc), 256);
-    const size_t off_un = o; o = align_up(o + nunit * sizeof(UnitDesc), 256);
     const size_t off_err = o; o += 256;
+    const size_t off_ctr = o; o += 256;
     sc.meta.ensure(o);
+    sc.meta.fresh = true;
     void* meta = sc.meta.ptr;
     SegDesc* dseg = at<SegDesc>(meta, off_seg);
     ChunkDesc* dch = at<ChunkDesc>(meta, off_ch);
-    UnitDesc* dun = at<UnitDesc>(meta, off_un);
     uint32_t* derr = at<uint32_t>(meta, off_err);
+    LevelCounters* dctr = at<LevelCounters>(meta, off_ctr);
     ModelDev hm{};
     hm.A = h_model->a; hm.B = h_model->b; hm.pivot_ok = h_model->pivot_ok;
-    hm.kind = h_model->kind; hm.D = h_model->D; hm.capped = h_model->capped; hm.k_eff = k_eff;
+    hm.kind = h_model->kind; hm.D = h_model->D; hm.capped = h_model->capped; hm.k_eff = k;
     ModelDev* dmod = at<ModelDev>(meta, ML.models);
     ck(cudaMemcpyAsync(dmod, &hm, sizeof(hm), cudaMemcpyHostToDevice, st));
     ck(cudaMemsetAsync(derr, 0, 16, st));
-    k_init_root<<<std::max<uint32_t>(1, (nchunk + 255) / 256), 256, 0, st>>>(dseg, dch, dun, n, 0,
+    ck(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
+    ck(cudaMemsetAsync(at<uint64_t>(meta, ML.status), 0, (size_t)nchunk * k * 8, st));
+    k_init_root<<<std::max<uint32_t>(1, (nchunk + 255) / 256), 256, 0, st>>>(dseg, dch, n, 0,
                                                                           ck_keys, 0u);
     ck_launch();
-    uint32_t* chunk_hist = at<uint32_t>(meta, ML.chunk_hist);
-    uint64_t* chunk_rep = at<uint64_t>(meta, ML.chunk_rep);
-    uint32_t* unit_cnt = at<uint32_t>(meta, ML.unit_cnt);
-    uint64_t* unit_rep = at<uint64_t>(meta, ML.unit_rep);
-    uint32_t* seg_tot = at<uint32_t>(meta, ML.seg_tot);
-    uint64_t* seg_rep = at<uint64_t>(meta, ML.seg_rep);
-    uint64_t* seg_dst = at<uint64_t>(meta, ML.seg_dst);
-    const uint64_t* in = static_cast<const uint64_t*>(d_in);
+    LevelArgs la{};
+    la.src = static_cast<const uint64_t*>(d_in); la.segs = dseg; la.chunks = dch;
+    la.models = dmod; la.k = k; la.base_case = 0; la.level = 0; la.chunk_keys = ck_keys;
+    la.ticket = &dctr->ticket;
+    la.status = at<uint64_t>(meta, ML.status);
+    la.cnt_agg = at<uint32_t>(meta, ML.cnt_agg);
+    la.rep_agg = at<uint64_t>(meta, ML.rep_agg);
+    la.chunk_pre = at<uint32_t>(meta, ML.chunk_pre);
+    la.seg_dst = at<uint64_t>(meta, ML.seg_dst);
+    la.seg_tot = nullptr;
+    bool wrapped = false;
+    la.epoch = next_epoch(&wrapped);
+    la.err = derr;
+    la.check_nan = 0;
+    la.ids = d_bucket_ids;
+    la.single_offsets = d_offsets;
     uint64_t* out = static_cast<uint64_t*>(d_out);
-    uint32_t log2k = 0;
-    while ((1u << log2k) < k) ++log2k;
-    if (log2k < 2) log2k = 2;
     auto body = [&](auto f64tag) {
       constexpr bool F64 = decltype(f64tag)::value;
       set_attrs<F64>();
-      k_classify_hist<F64><<<nchunk, kTileThreads, classify_smem(k), st>>>(
-          in, dch, dseg, dmod, k, chunk_hist, chunk_rep, derr, 0, d_bucket_ids, 0);
+      k_classify_scan<F64><<<nchunk, kCThreads, classify_smem(k), st>>>(la);
       ck_launch();
-      k_unit_reduce<<<col_blocks(nunit, k), 256, 0, st>>>(dun, nunit, k, chunk_hist, chunk_rep,
-                                                           unit_cnt, unit_rep);
-      ck_launch();
-      k_seg_scan<<<col_blocks(1, k), 256, 0, st>>>(dseg, 1, k, unit_cnt, unit_rep, seg_tot,
-                                                    seg_rep);
-      ck_launch();
-      k_single_offsets<<<1, kOffThreads, 0, st>>>(seg_tot, k, k_eff, seg_dst, d_offsets);
-      ck_launch();
-      k_chunk_prefix<<<col_blocks(nunit, k), 256, 0, st>>>(dun, nunit, k, unit_cnt, chunk_hist);
-      ck_launch();
-      launch_scatter<F64>(log2k, dim3(nchunk), scatter_smem(k), st, in, out, out, dch, dmod, k,
-                          chunk_hist, seg_dst, derr);
+      launch_scatter<F64>(nchunk, st, la.src, out, out, dch, dmod, k, la.chunk_pre, la.seg_dst,
+                          derr);
     };
     if (t == IPLS_KEY_F64) body(std::true_type{}); else body(std::false_type{});
     ck(cudaStreamSynchronize(st));

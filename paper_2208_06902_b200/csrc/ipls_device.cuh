@@ -24,7 +24,6 @@ struct SegDesc {            // one partition work item of a level (segment of th
   uint32_t S;               // sample size S(m) (R1, R19)
   uint64_t sample_off;      // offset of its sample in the level's sample buffer
   uint32_t chunk_first, nchunks;
-  uint32_t unit_first, nunits;
   uint32_t flags;           // kSegForceEq3
   uint32_t pad;
 };
@@ -40,10 +39,6 @@ struct ChunkDesc {          // a run of <= CHUNK keys of one segment, processed 
   uint32_t len, seg;
 };
 
-struct UnitDesc {           // up to 32 consecutive chunks of one segment (column-scan unit)
-  uint32_t seg, chunk_first, nch, pad;
-};
-
 struct Window {             // contiguous run of whole final segments for the base case
   uint64_t begin;
   uint32_t len, buf;        // buf: 0 = user array, 1 = scratch
@@ -56,8 +51,8 @@ struct Fill {               // homogeneous child that must be written into the u
 };
 
 struct LevelCounters {      // device-side counters of the level being built
-  uint32_t n_segs, n_chunks, n_units, n_samples;
-  uint32_t n_windows, n_fills, err, pad;
+  uint32_t n_segs, n_chunks, max_S, n_samples;
+  uint32_t n_windows, n_fills, err, ticket;  // ticket: chunk order of this level's classify
   uint64_t keys;            // keys in next-level segments
   uint64_t win_keys;        // keys in this level's base-case windows
   uint64_t fill_keys;       // keys in this level's fills
@@ -86,25 +81,32 @@ __device__ __forceinline__ bool is_nan_bits(uint64_t bits) {
   return ((bits >> 52) & 0x7ff) == 0x7ff && (bits & 0xfffffffffffffull) != 0;
 }
 
-// P:394-402 with R7: 0 if !(y >= 0); k-1 if y >= k; floor(y) otherwise.
-__device__ __forceinline__ uint32_t linear_bucket(double v, double A, double B, double kd,
-                                                  uint32_t km1) {
-  double t = __dmul_rn(A, v);
-  double y = __dadd_rn(t, B);
-  if (!(y >= 0.0)) return 0u;
-  if (y >= kd) return km1;
-  return (uint32_t)y;  // cvt.rzi: 0 <= y < k so truncation == floor
+// P:394-402 with R7: 0 if !(y >= 0); k-1 if y >= k; floor(y) otherwise, y = RN(RN(A*v) + B).
+// cvt.rzi.u32.f64 (__double2uint_rz) truncates toward zero and saturates: y < 0 (also -inf,
+// -0.0 and (-1, 0)) gives 0, NaN gives 0, y >= 2^32 gives 2^32-1; min(., k-1) then clamps
+// the top.  That is exactly the three-way rule above, in two instructions.
+__device__ __forceinline__ uint32_t linear_bucket(double v, double A, double B, uint32_t km1) {
+  const double y = __dadd_rn(__dmul_rn(A, v), B);
+  return min(__double2uint_rz(y), km1);
 }
 
-template <bool F64>
-__device__ __forceinline__ uint32_t bucket_of(uint64_t bits, const ModelDev& md, double kd,
-                                              uint32_t km1) {
-  if (md.kind == kModelEq3) {
-    uint64_t o = ok_of<F64>(bits);
-    return (o < md.pivot_ok) ? 0u : ((o == md.pivot_ok) ? 1u : 2u);
+// Bucket function with the model kind fixed at compile time (the kind is uniform per chunk).
+template <bool F64, bool EQ3>
+struct Bucketer {
+  double A, B;
+  uint64_t piv;
+  uint32_t km1;
+  __device__ __forceinline__ explicit Bucketer(const ModelDev& md, uint32_t k)
+      : A(md.A), B(md.B), piv(md.pivot_ok), km1(k - 1) {}
+  __device__ __forceinline__ uint32_t operator()(uint64_t bits) const {
+    if constexpr (EQ3) {
+      const uint64_t o = ok_of<F64>(bits);
+      return (o < piv) ? 0u : ((o == piv) ? 1u : 2u);
+    } else {
+      return linear_bucket(value_of<F64>(bits), A, B, km1);
+    }
   }
-  return linear_bucket(value_of<F64>(bits), md.A, md.B, kd, km1);
-}
+};
 
 // SplitMix64 output function (R18).
 __device__ __forceinline__ uint64_t sm64(uint64_t z) {
