@@ -110,7 +110,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Params {
   uint64_t n;
   uint32_t k, B, chunk_keys;
-  uint32_t cap_segs, cap_chunks, cap_samples, cap_wins, cap_fills;
+  uint32_t cap_segs, cap_chunks, cap_samples, cap_wins, cap_wbig, cap_fills;
 };
 
 uint32_t pick_chunk_keys(uint64_t n) {
@@ -130,12 +130,17 @@ Params make_params(uint64_t n, uint32_t k, uint32_t B) {
   const uint64_t chunks = n / p.chunk_keys + segs + 1;
   const uint64_t smax = sample_size(n, k);
   uint64_t samples = std::min<uint64_t>(n / 2 + 8, segs * smax + 8);
-  uint64_t wins = std::min<uint64_t>(n + 1, n / ((uint64_t)B + 1) + n / kWindowNominal + 2 * segs) + 16;
+  // small windows: greedy packing makes consecutive windows of a run exceed kWBCap keys
+  // together, runs are cut by breakers (<= n / (kWBCap + 1) big base children and <= segs
+  // partition/homogeneous children per level) and by segment ends
+  uint64_t wins = std::min<uint64_t>(n + 1, 2 * n / kWBCap + 2 * (n / (kWBCap + 1)) + 4 * segs) + 64;
+  uint64_t wbig = std::min<uint64_t>(n / (kWBCap + 1), 2 * n / kBaseMax + 2 * (n / (kWBCap + 1)) + 4 * segs) + 64;
   uint64_t fills = n / ((uint64_t)B + 1) + 16;
   p.cap_segs = (uint32_t)segs;
   p.cap_chunks = (uint32_t)chunks;
   p.cap_samples = (uint32_t)samples;
   p.cap_wins = (uint32_t)wins;
+  p.cap_wbig = (uint32_t)wbig;
   p.cap_fills = (uint32_t)fills;
   return p;
 }
@@ -143,7 +148,7 @@ Params make_params(uint64_t n, uint32_t k, uint32_t B) {
 // Fixed part of the workspace: scratch keys + descriptors of two levels + windows/fills of
 // two levels + counters.  The k-scaled per-level metadata is carved after it.
 struct FixedLayout {
-  size_t scratch, segs[2], chunks[2], wins[2], fills[2], ctr[2], err, total;
+  size_t scratch, segs[2], chunks[2], wins[2], wbig[2], fills[2], ctr[2], err, tickets, total;
 };
 
 FixedLayout fixed_layout(const Params& p) {
@@ -155,10 +160,12 @@ FixedLayout fixed_layout(const Params& p) {
     L.segs[i] = take((size_t)p.cap_segs * sizeof(SegDesc));
     L.chunks[i] = take((size_t)p.cap_chunks * sizeof(ChunkDesc));
     L.wins[i] = take((size_t)p.cap_wins * sizeof(Window));
+    L.wbig[i] = take((size_t)p.cap_wbig * sizeof(Window));
     L.fills[i] = take((size_t)p.cap_fills * sizeof(Fill));
     L.ctr[i] = take(sizeof(LevelCounters));
   }
   L.err = take(16);
+  L.tickets = take(64);
   L.total = o;
   return L;
 }
@@ -258,8 +265,20 @@ void launch_scatter(uint32_t nchunk, cudaStream_t st, const uint64_t* src, uint6
                                                              chunk_pre, seg_dst, err);
   ck_launch();
 }
-size_t classify_smem(uint32_t k) { return (size_t)k * 8 + (size_t)k * 12; }
-size_t base_smem() { return (size_t)kBaseMax * 12; }
+size_t classify_smem(uint32_t k) {
+  return std::max((size_t)k * 8 + (size_t)k * 12, win_scratch_bytes(k));
+}
+size_t warp_base_smem() { return kWBSmemPerWarp * kWBWarps; }
+size_t base_smem() { return (size_t)2 * kPBStride * 8 + (size_t)kBaseMax * 12; }
+int g_num_sms = 0;
+uint32_t num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    ck(cudaGetDevice(&dev));
+    ck(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return (uint32_t)g_num_sms;
+}
 uint32_t fit_cap(uint32_t maxS) {
   uint32_t c = 64;
   while (c < maxS) c <<= 1;
@@ -273,8 +292,12 @@ void set_attrs() {
   if (done) return;
   ck(cudaFuncSetAttribute(k_gather_fit<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)fit_smem(kFitMaxS)));
-  ck(cudaFuncSetAttribute(k_base_sort<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ck(cudaFuncSetAttribute(k_base_sort<F64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)base_smem()));
+  ck(cudaFuncSetAttribute(k_base_sort<F64, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)base_smem()));
+  ck(cudaFuncSetAttribute(k_base_warp<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)warp_base_smem()));
   ck(cudaFuncSetAttribute(k_classify_scan<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)classify_smem(kMaxK)));
   ck(cudaFuncSetAttribute(k_scatter<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -310,7 +333,9 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     ck(cudaMemcpyAsync(dw, &w, sizeof(Window), cudaMemcpyHostToDevice, st));
     {
       IPLS_PROF("base_sort", 16.0 * n);
-      k_base_sort<F64><<<1, kBaseThreads, base_smem(), st>>>(dw, keys, scr, d_err, F64 ? 1 : 0);
+      uint32_t* tk = at<uint32_t>(fixed, FL.tickets);
+      ck(cudaMemsetAsync(tk, 0, 4, st));
+      k_base_sort<F64, F64><<<1, kPBThreads, base_smem(), st>>>(dw, 1, tk, keys, scr, d_err);
       ck_launch();
     }
     ck(cudaMemcpyAsync(&h_ctr[1].err, d_err, 4, cudaMemcpyDeviceToHost, st));
@@ -339,6 +364,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     LevelCounters* cctr = at<LevelCounters>(fixed, FL.ctr[cur]);
     LevelCounters* nctr = at<LevelCounters>(fixed, FL.ctr[nxt]);
     Window* wins = at<Window>(fixed, FL.wins[cur]);
+    Window* wbig = at<Window>(fixed, FL.wbig[cur]);
     Fill* fills = at<Fill>(fixed, FL.fills[cur]);
 
     // per-level metadata, sized by this level's actual counts
@@ -394,6 +420,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     la.nctr = nctr;
     la.cap_segs = p.cap_segs; la.cap_chunks = p.cap_chunks; la.cap_samples = p.cap_samples;
     la.wins = wins; la.cap_wins = p.cap_wins; la.fills = fills; la.cap_fills = p.cap_fills;
+    la.wins_big = wbig; la.cap_wbig = p.cap_wbig;
     {
       IPLS_PROF("classify_scan", 8.0 * level_keys);
       k_classify_scan<F64><<<nchunk, kCThreads, classify_smem(k), st>>>(la);
@@ -452,8 +479,17 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
 
     // base case of this level's base children, fills of its homogeneous children
     if (c.n_windows) {
-      IPLS_PROF("base_sort", 16.0 * c.win_keys);
-      k_base_sort<F64><<<c.n_windows, kBaseThreads, base_smem(), st>>>(wins, keys, scr, d_err, 0);
+      IPLS_PROF("base_warp", 16.0 * c.win_keys);
+      k_base_warp<F64><<<std::min((c.n_windows + kWBWarps - 1) / kWBWarps, num_sms()),
+                         kWBWarps * 32, warp_base_smem(), st>>>(wins, c.n_windows, keys, scr);
+      ck_launch();
+    }
+    if (c.n_wbig) {
+      IPLS_PROF("base_sort", 16.0 * c.wbig_keys);
+      uint32_t* tk = at<uint32_t>(fixed, FL.tickets);
+      ck(cudaMemsetAsync(tk, 0, 4, st));
+      k_base_sort<F64, false><<<std::min(c.n_wbig, num_sms()), kPBThreads, base_smem(), st>>>(
+          wbig, c.n_wbig, tk, keys, scr, d_err);
       ck_launch();
     }
     if (c.n_fills) {

@@ -54,7 +54,9 @@ struct LevelCounters {      // device-side counters of the level being built
   uint32_t n_segs, n_chunks, max_S, n_samples;
   uint32_t n_windows, n_fills, err, ticket;  // ticket: chunk order of this level's classify
   uint64_t keys;            // keys in next-level segments
-  uint64_t win_keys;        // keys in this level's base-case windows
+  uint32_t n_wbig, pad;     // single-child base windows above the warp-window cap
+  uint64_t win_keys;        // keys in this level's small base-case windows
+  uint64_t wbig_keys;       // keys in this level's big base-case windows
   uint64_t fill_keys;       // keys in this level's fills
 };
 
@@ -107,6 +109,36 @@ struct Bucketer {
     }
   }
 };
+
+// ---- async bulk copies (TMA 1-D, cp.async.bulk) and mbarriers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// global -> shared, completion counted on `bar` (bytes and both addresses 16-byte aligned)
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 // SplitMix64 output function (R18).
 __device__ __forceinline__ uint64_t sm64(uint64_t z) {

@@ -24,10 +24,16 @@ constexpr int kSRounds = 16;  // keys per thread per tile
 constexpr int kSTile = kSThreads * kSRounds;   // 4096
 constexpr int kFitThreads = 1024;
 constexpr int kFitMaxS = 8192;
-constexpr int kBaseThreads = 512;
 constexpr int kBaseMax = 8192;                 // keys per base-case window (W + B)
-constexpr uint32_t kWindowNominal = 4096;
 constexpr uint32_t kMaxK = 1024;
+// small-window base case (k_base_warp)
+constexpr int kWBCap = 512;                      // keys per warp window
+constexpr int kWBBinsPerKey = 2;
+constexpr int kWBBins = kWBBinsPerKey * kWBCap;  // fine bins per warp
+constexpr int kWBWarps = 12;                     // warps per CTA, one CTA per SM
+constexpr int kWBStride = kWBCap + 4;            // keys per prefetch buffer (+ alignment slack)
+constexpr size_t kWBSmemPerWarp =
+    (size_t)2 * kWBStride * 8 + kWBCap * 8 + kWBCap * 4 + (kWBBins + 32) * 4;
 constexpr uint32_t kFineOverflow = 32;          // fine-bin load that triggers the bitonic fallback
 
 // ------------------------------------------------------------------------------------
@@ -201,7 +207,7 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
     uint32_t level, uint32_t k, uint32_t cap, uint64_t* __restrict__ samples_out,
     ModelDev* __restrict__ models, const uint64_t* __restrict__ presorted_ok) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* a = reinterpret_cast<uint64_t*>(smraw);   // cap
   uint64_t* tmp = a + cap;                             // cap
   uint32_t* fh = reinterpret_cast<uint32_t*>(tmp + cap);  // cap
@@ -307,8 +313,10 @@ struct LevelArgs {
   ChunkDesc* nchunks;
   LevelCounters* nctr;
   uint32_t cap_segs, cap_chunks, cap_samples;
-  Window* wins;
+  Window* wins;        // small windows (<= kWBCap keys): k_base_warp
   uint32_t cap_wins;
+  Window* wins_big;    // single base children above kWBCap: k_base_sort
+  uint32_t cap_wbig;
   Fill* fills;
   uint32_t cap_fills;
 };
@@ -348,16 +356,125 @@ __device__ void emit_segment(const LevelArgs& a, uint64_t begin, uint32_t m, uin
 struct OffSmem {
   uint32_t warp[40];
   uint32_t res[8];
-  uint32_t basey[kMaxK];
-  uint32_t wid[kMaxK];
-  uint32_t wbeg[kMaxK];
-  uint32_t wend[kMaxK];
 };
+// Window-formation scratch (aliases the classify CTA's dynamic smem at the segment's end).
+constexpr uint32_t kWinArrays = 8;  // start, end, brk_incl, sm_incl, small_idx, jump, J, mark
+__host__ __device__ constexpr size_t win_scratch_bytes(uint32_t k) {
+  return (size_t)kWinArrays * (k + 1) * 4;
+}
+
+// Greedy left-to-right packing of the children selected by `sel` into windows of <= cap keys
+// (a window is a contiguous run of selected and empty children; any other non-empty child
+// breaks it).  jump(c) = last child reachable from selected child c without a breaker and
+// within cap keys (binary search); J(c) = first selected child after jump(c); the window
+// starts are the orbit of the first selected child under J, marked by pointer doubling
+// (log2 k rounds).  Appends the windows to `out` (global counter `cnt`, keys to `keys`).
+__device__ void pack_windows(const LevelArgs& a, const SegDesc& sg, uint32_t k,
+                             const uint32_t (&bb)[kCBpt], const uint32_t (&base)[kCBpt],
+                             const uint32_t (&tot)[kCBpt], const bool (&sel)[kCBpt], uint32_t cap,
+                             uint32_t dstbuf, OffSmem& os, uint32_t* wsm, Window* out,
+                             uint32_t out_cap, uint32_t* cnt, uint64_t* keys) {
+  const uint32_t K1 = k + 1;
+  uint32_t* w_start = wsm;
+  uint32_t* w_end = wsm + K1;
+  uint32_t* w_brk = wsm + 2 * K1;
+  uint32_t* w_sm = wsm + 3 * K1;
+  uint32_t* w_idx = wsm + 4 * K1;
+  uint32_t* w_jump = wsm + 5 * K1;
+  uint32_t* w_J = wsm + 6 * K1;
+  uint32_t* w_mark = wsm + 7 * K1;
+  uint32_t nbrk = 0, nsel = 0;
+#pragma unroll
+  for (int q = 0; q < kCBpt; ++q) {
+    nbrk += (bb[q] < k && tot[q] && !sel[q]) ? 1u : 0u;
+    nsel += sel[q] ? 1u : 0u;
+  }
+  uint32_t t_sel;
+  uint32_t brk_run = block_exclusive_scan<kCThreads>(nbrk, os.warp, nullptr);
+  uint32_t sel_run = block_exclusive_scan<kCThreads>(nsel, os.warp, &t_sel);
+  if (t_sel == 0) return;  // block-uniform
+#pragma unroll
+  for (int q = 0; q < kCBpt; ++q) {
+    if (bb[q] < k) {
+      brk_run += (tot[q] && !sel[q]) ? 1u : 0u;
+      if (sel[q]) w_idx[sel_run] = bb[q];
+      sel_run += sel[q] ? 1u : 0u;
+      w_start[bb[q]] = base[q];
+      w_end[bb[q]] = base[q] + tot[q];
+      w_brk[bb[q]] = brk_run;
+      w_sm[bb[q]] = sel_run;
+      w_mark[bb[q]] = 0u;
+    }
+  }
+  if (threadIdx.x == 0) { w_J[k] = k; w_mark[k] = 0u; }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kCBpt; ++q) {
+    if (sel[q]) {
+      const uint32_t c = bb[q], st0 = base[q], bk0 = w_brk[c];
+      uint32_t lo = c, hi = k;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (w_brk[mid] == bk0 && w_end[mid] - st0 <= cap) lo = mid; else hi = mid;
+      }
+      w_jump[c] = lo;
+      const uint32_t m = w_sm[lo];
+      w_J[c] = (m < t_sel) ? w_idx[m] : k;
+    } else if (bb[q] < k) {
+      w_J[bb[q]] = k;
+    }
+  }
+  if (threadIdx.x == 0) w_mark[w_idx[0]] = 1u;
+  __syncthreads();
+  for (uint32_t span = 1; span < t_sel; span <<= 1) {
+    uint32_t mk[kCBpt], jj[kCBpt], j2[kCBpt];
+#pragma unroll
+    for (int q = 0; q < kCBpt; ++q) {
+      mk[q] = 0; jj[q] = k; j2[q] = k;
+      if (bb[q] < k) {
+        mk[q] = w_mark[bb[q]];
+        jj[q] = w_J[bb[q]];
+        j2[q] = w_J[jj[q]];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kCBpt; ++q) {
+      if (mk[q] && jj[q] < k) w_mark[jj[q]] = 1u;
+      if (bb[q] < k) w_J[bb[q]] = j2[q];
+    }
+    __syncthreads();
+  }
+  uint32_t nw = 0;
+#pragma unroll
+  for (int q = 0; q < kCBpt; ++q) nw += (sel[q] && w_mark[bb[q]]) ? 1u : 0u;
+  uint32_t t_w;
+  uint32_t w_off = block_exclusive_scan<kCThreads>(nw, os.warp, &t_w);
+  if (threadIdx.x == 0) os.res[4] = atomicAdd(cnt, t_w);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kCBpt; ++q) {
+    if (sel[q] && w_mark[bb[q]]) {
+      const uint32_t gi = os.res[4] + w_off++;
+      if (gi < out_cap) {
+        Window wv;
+        wv.begin = sg.begin + base[q];
+        wv.len = w_end[w_jump[bb[q]]] - base[q];
+        wv.buf = dstbuf;
+        out[gi] = wv;
+        atomicAdd((unsigned long long*)keys, (unsigned long long)wv.len);
+      } else {
+        atomicOr(a.err, kErrOverflow);
+      }
+    }
+  }
+  __syncthreads();  // scratch is reused by the next packing
+}
 
 __device__ void segment_offsets(const LevelArgs& a, uint32_t s, const SegDesc& sg,
                                 const ModelDev& md, const uint32_t (&tot)[kCBpt],
                                 const uint32_t (&inh)[kCBpt], const uint64_t (&rep)[kCBpt],
-                                OffSmem& os) {
+                                OffSmem& os, uint32_t* wsm) {
   const uint32_t k = a.k;
   uint32_t bb[kCBpt], base[kCBpt];
   uint32_t x = 0;
@@ -444,57 +561,21 @@ __device__ void segment_offsets(const LevelArgs& a, uint32_t s, const SegDesc& s
     }
   }
   if (stuck) return;  // block-uniform
-  // ---- base-case windows: maximal runs of base/empty children within one W-window ----
-  bool basey[kCBpt];
-  uint32_t wid[kCBpt];
-#pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
-    basey[q] = (bb[q] < k) && (cls[q] <= 1);
-    wid[q] = base[q] / kWindowNominal;
-    if (bb[q] < k) { os.basey[bb[q]] = basey[q]; os.wid[bb[q]] = wid[q]; }
-  }
-  __syncthreads();
-  uint32_t start[kCBpt], nst = 0;
-#pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
-    start[q] = 0;
-    if (basey[q])
-      start[q] = (bb[q] == 0) || !os.basey[bb[q] - 1] || os.wid[bb[q] - 1] != wid[q];
-    nst += start[q];
-  }
-  uint32_t t_win;
-  uint32_t o_win = block_exclusive_scan<kCThreads>(nst, os.warp, &t_win);
-  uint32_t widx[kCBpt];
+  // ---- base-case windows ----
+  // Base children of <= kWBCap keys ("small") are packed into windows of <= kWBCap keys
+  // (sorted by k_base_warp); base children above kWBCap ("big") into windows of <= kBaseMax
+  // keys (k_base_sort).  Every other child breaks a window.
   {
-    uint32_t run = o_win;
+    bool small[kCBpt], bigb[kCBpt];
 #pragma unroll
     for (int q = 0; q < kCBpt; ++q) {
-      run += start[q];
-      widx[q] = run - 1;
-      if (start[q]) { os.wbeg[widx[q]] = base[q]; os.wend[widx[q]] = base[q]; }
+      small[q] = bb[q] < k && cls[q] == 1 && tot[q] <= (uint32_t)kWBCap;
+      bigb[q] = bb[q] < k && cls[q] == 1 && tot[q] > (uint32_t)kWBCap;
     }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < kCBpt; ++q)
-    if (basey[q] && tot[q]) atomicMax(&os.wend[widx[q]], base[q] + tot[q]);
-  if (threadIdx.x == 0 && t_win) os.res[4] = atomicAdd(&a.nctr->n_windows, t_win);
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
-    if (start[q]) {
-      uint32_t gi = os.res[4] + widx[q];
-      if (gi < a.cap_wins) {
-        Window wv;
-        wv.begin = sg.begin + os.wbeg[widx[q]];
-        wv.len = os.wend[widx[q]] - os.wbeg[widx[q]];
-        wv.buf = dstbuf;
-        a.wins[gi] = wv;
-        if (wv.len) atomicAdd((unsigned long long*)&a.nctr->win_keys, (unsigned long long)wv.len);
-      } else {
-        atomicOr(a.err, kErrOverflow);
-      }
-    }
+    pack_windows(a, sg, k, bb, base, tot, small, (uint32_t)kWBCap, dstbuf, os, wsm, a.wins,
+                 a.cap_wins, &a.nctr->n_windows, &a.nctr->win_keys);
+    pack_windows(a, sg, k, bb, base, tot, bigb, (uint32_t)kBaseMax, dstbuf, os, wsm, a.wins_big,
+                 a.cap_wbig, &a.nctr->n_wbig, &a.nctr->wbig_keys);
   }
   // ---- homogeneous children that land in scratch must be filled into the user array ----
   uint32_t nf = 0;
@@ -586,7 +667,7 @@ __device__ __forceinline__ void classify_dispatch(const LevelArgs& a, const Chun
 
 template <bool F64>
 __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   const uint32_t k = a.k;
   uint64_t* rep = reinterpret_cast<uint64_t*>(smraw);  // k
   uint32_t* hist = reinterpret_cast<uint32_t*>(rep + k);
@@ -688,7 +769,10 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
       rp[q] = ref;
     }
   }
-  if (last) segment_offsets(a, ch.seg, sg, md, tot, inh, rp, os);
+  if (last) {
+    __syncthreads();  // the histogram smem becomes window-formation scratch
+    segment_offsets(a, ch.seg, sg, md, tot, inh, rp, os, reinterpret_cast<uint32_t*>(smraw));
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -882,7 +966,7 @@ __global__ __launch_bounds__(kSThreads, 2) void k_scatter(
     const ModelDev* __restrict__ models, uint32_t k, const uint32_t* __restrict__ chunk_pre,
     const uint64_t* __restrict__ seg_dst, const uint32_t* __restrict__ err) {
   if (*((volatile const uint32_t*)err) & kErrNan) return;
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   const ChunkDesc ch = chunks[blockIdx.x];
   const ModelDev md = models[ch.seg];
   if (md.kind == kModelEq3)
@@ -892,148 +976,529 @@ __global__ __launch_bounds__(kSThreads, 2) void k_scatter(
 }
 
 // ------------------------------------------------------------------------------------
-// Base case: sort one window of whole final segments (<= 8192 keys) by ordering key
-// and write it to the user array.  Buckets are range-ordered (the model is monotone, R7),
-// so sorting a window of consecutive final segments sorts each of them; any exact sort
-// gives the identical bytes (R13).
-// Keys stay in registers (16 per thread).  Fine bin of a key = its position on a linear
-// map of [min, max] in ordering-key space onto len bins (windows at the last level span a
-// narrow, locally smooth range), through a 256-bin coarse histogram only when the window
-// spans more than two binades.  One counting pass places the keys into smem; bins hold ~1
-// key and are finished by insertion sort; windows whose bins overflow take a bitonic sort.
-constexpr int kBaseItems = kBaseMax / kBaseThreads;  // 16
+// Base case: sort windows of whole final segments (<= 8192 keys) by ordering key and
+// write them to the user array.  Buckets are range-ordered (the model is monotone, R7), so
+// sorting a window of consecutive final segments sorts each of them; any exact sort gives the
+// identical bytes (R13).
+//
+// Persistent kernel, one CTA of 1024 threads per SM, windows taken by atomic ticket.  While a
+// window is sorted, the next one streams into the other smem buffer with one TMA bulk copy
+// (cp.async.bulk, mbarrier completion), so DRAM latency is off the critical path.  The keys
+// of the current window move to registers (8 per thread) and their buffer becomes the
+// placement array.
+//
+// Sort = interpolation sort in ordering-key space: a 256-bin coarse histogram of
+// (ok - min) >> sh gives each coarse bin as many fine bins as it holds keys; the fine bin of
+// a key is its coarse bin's first fine bin plus its fractional position inside the coarse bin
+// times the coarse count (32-bit fraction, one IMAD.HI).  A counting pass places the keys bin
+// by bin; every thread then insertion-sorts the contiguous range of its 8 fine bins (keys of
+// different bins are already ordered, so only in-bin inversions move).  Windows whose fine
+// bins overflow (> kFineOverflow keys: adversarial clusters) take a bitonic sort.
+constexpr int kPBThreads = 1024;
+constexpr int kPBItems = kBaseMax / kPBThreads;  // 8
+constexpr int kPBStride = kBaseMax + 4;          // keys per smem buffer (+ alignment slack)
 
-template <bool F64>
-__global__ __launch_bounds__(kBaseThreads, 2) void k_base_sort(
-    const Window* __restrict__ wins, uint64_t* __restrict__ user, const uint64_t* __restrict__ scr,
-    uint32_t* __restrict__ err, int check_nan) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  uint64_t* tmp = reinterpret_cast<uint64_t*>(smraw);             // kBaseMax
-  uint32_t* fh = reinterpret_cast<uint32_t*>(tmp + kBaseMax);      // kBaseMax
-  __shared__ SortSmem ss;
-  const Window wv = wins[blockIdx.x];
-  const uint32_t len = wv.len;
-  if (len == 0) return;
-  const uint64_t* srcp = (wv.buf ? scr : user) + wv.begin;
-  uint64_t* dst = user + wv.begin;
+struct BaseSmem {
+  uint32_t cinfo[256];   // coarse bin: first fine bin | count << 16
+  uint64_t red[2 * (kPBThreads / 32)];  // per-warp min, then per-warp max
+  uint32_t warp[40];
+  uint64_t mbar[2];
+  uint32_t win[2];
+};
+
+__device__ __forceinline__ uint32_t base_fine_bin(uint64_t d, int sh, const uint32_t* cinfo) {
+  const uint32_t ci = cinfo[(uint32_t)(d >> sh)];
+  uint32_t f = ci & 0xffffu;
+  if (sh > 0) f += __umulhi((uint32_t)((d << (64 - sh)) >> 32), ci >> 16);
+  return f;
+}
+
+// Window geometry for the bulk copy: keys [head, head + body) are 16-byte aligned in global
+// memory and land at smem buf[2 ...]; the 0-1 keys before and after (head, tail) are loaded
+// by thread 0 and stored around the body, so key i of the window sits at buf[2 - head + i].
+struct WinGeom {
+  uint32_t head, body, tail;
+};
+__device__ __forceinline__ WinGeom win_geom(const uint64_t* g, uint32_t len) {
+  WinGeom w;
+  w.head = ((reinterpret_cast<uintptr_t>(g) & 15u) != 0 && len > 0) ? 1u : 0u;
+  w.body = (len - w.head) & ~1u;
+  w.tail = len - w.head - w.body;
+  return w;
+}
+
+// Sort the keys v[] (ordering keys; slots j*NT+tid < len valid) of one window.  On return
+// the sorted (ok - min) values are in OUT[0, len) (OUT = B2, or B after the bitonic fallback)
+// and `mn` holds min.  B, B2: kBaseMax u64 smem; fh: kBaseMax u32 smem.  Ends with a barrier.
+#ifdef IPLS_BASE_TIMING  // dev harness only: per-phase clock accumulation by thread 0
+__device__ unsigned long long g_base_phase[16];
+#define BASE_TICK(N)                                                         \
+  do {                                                                       \
+    if (threadIdx.x == 0) {                                                  \
+      const long long t_ = clock64();                                        \
+      atomicAdd(&g_base_phase[N], (unsigned long long)(t_ - t_prev_));       \
+      t_prev_ = t_;                                                          \
+    }                                                                        \
+  } while (0)
+#else
+#define BASE_TICK(N)
+#endif
+template <int NT, int ITEMS>
+__device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint64_t* B, uint64_t* B2,
+                                       uint32_t* fh, BaseSmem& ss, uint64_t& mn_out,
+                                       long long& t_prev_) {
+  constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  uint64_t v[kBaseItems];
   uint64_t mn = ~0ull, mx = 0ull;
-  int nan_seen = 0;
 #pragma unroll
-  for (int j = 0; j < kBaseItems; ++j) {
-    const uint32_t i = j * kBaseThreads + threadIdx.x;
-    v[j] = 0;
-    if (i < len) {
-      const uint64_t bits = __ldcs(srcp + i);
-      if (F64 && check_nan && is_nan_bits(bits)) nan_seen = 1;
-      v[j] = ok_of<F64>(bits);
-      mn = min(mn, v[j]);
-      mx = max(mx, v[j]);
-    }
+  for (int j = 0; j < ITEMS; ++j) {
+    if (j * NT + threadIdx.x < len) { mn = min(mn, v[j]); mx = max(mx, v[j]); }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
-  if (lane == 0) { ss.red[wp] = mn; ss.red[32 + wp] = mx; }
-  for (uint32_t i = threadIdx.x; i < len; i += kBaseThreads) fh[i] = 0u;
-  for (uint32_t c = threadIdx.x; c < 256; c += kBaseThreads) ss.ccnt[c] = 0u;
-  if (check_nan) {
-    if (__syncthreads_or(nan_seen)) {
-      if (threadIdx.x == 0) atomicOr(err, kErrNan);
-      return;
-    }
-  } else {
-    __syncthreads();
-  }
-  mn = ss.red[0]; mx = ss.red[32];
+  if (lane == 0) { ss.red[wp] = mn; ss.red[NW + wp] = mx; }
+  for (uint32_t c = threadIdx.x; c < 256; c += NT) ss.cinfo[c] = 0u;
+  {
+    uint4* f4 = reinterpret_cast<uint4*>(fh) + threadIdx.x * (ITEMS / 4);
 #pragma unroll
-  for (int w = 1; w < kBaseThreads / 32; ++w) { mn = min(mn, ss.red[w]); mx = max(mx, ss.red[32 + w]); }
-  if (mn == mx) {  // constant window: already sorted
-    if (wv.buf) {
-#pragma unroll
-      for (int j = 0; j < kBaseItems; ++j) {
-        const uint32_t i = j * kBaseThreads + threadIdx.x;
-        if (i < len) __stcs(dst + i, bits_of_ok<F64>(v[j]));
-      }
-    }
-    return;
-  }
-  const uint64_t range = mx - mn;
-  const int bl = 64 - __clzll((long long)range);
-  const bool coarse = bl > 54;  // more than two binades of doubles
-  uint32_t f[kBaseItems];
-  int sh = 0;
-  if (coarse) {
-    sh = bl - 8;
-#pragma unroll
-    for (int j = 0; j < kBaseItems; ++j) {
-      const uint32_t i = j * kBaseThreads + threadIdx.x;
-      if (i < len) atomicAdd(&ss.ccnt[(uint32_t)((v[j] - mn) >> sh)], 1u);
-    }
-    __syncthreads();
-    uint32_t cc = (threadIdx.x < 256) ? ss.ccnt[threadIdx.x] : 0u;
-    uint32_t ex = block_exclusive_scan<kBaseThreads>(cc, ss.warp, nullptr);
-    if (threadIdx.x < 256) ss.coff[threadIdx.x] = ex;
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kBaseItems; ++j) {
-      const uint32_t i = j * kBaseThreads + threadIdx.x;
-      f[j] = (i < len) ? fine_bin(v[j], mn, sh, ss.coff, ss.ccnt) : 0u;
-    }
-  } else {
-    const int up = 64 - bl;  // (ok - mn) << up is the fraction of the range in [0, 1)
-#pragma unroll
-    for (int j = 0; j < kBaseItems; ++j) f[j] = (uint32_t)__umul64hi((v[j] - mn) << up, len);
-  }
-#pragma unroll
-  for (int j = 0; j < kBaseItems; ++j) {
-    const uint32_t i = j * kBaseThreads + threadIdx.x;
-    if (i < len) atomicAdd(&fh[f[j]], 1u);
+    for (int q = 0; q < ITEMS / 4; ++q) f4[q] = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
-  // exclusive scan of fh[0..len): thread t owns bins [t*16, t*16+16)
+  {
+    uint64_t a = ss.red[lane & (NW - 1)], b = ss.red[NW + (lane & (NW - 1))];
+#pragma unroll
+    for (int o = NW / 2; o > 0; o >>= 1) {
+      a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    mn = a; mx = b;
+  }
+  BASE_TICK(2);
+  mn_out = mn;
+  if (mn == mx) {  // constant window: every key is mn
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j)
+      if (j * NT + threadIdx.x < len) B2[j * NT + threadIdx.x] = 0;
+    __syncthreads();
+    return B2;
+  }
+  const int bl = 64 - __clzll((long long)(mx - mn));
+  const int sh = bl > 8 ? bl - 8 : 0;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    v[j] -= mn;  // v now holds ok - min
+    if (j * NT + threadIdx.x < len) atomicAdd(&ss.cinfo[(uint32_t)(v[j] >> sh)], 1u);
+  }
+  __syncthreads();
+  BASE_TICK(3);
+  {
+    uint32_t cc = 0;
+    if (threadIdx.x < 256) cc = ss.cinfo[threadIdx.x];
+    const uint32_t ex = block_exclusive_scan<NT>(cc, ss.warp, nullptr);
+    if (threadIdx.x < 256) ss.cinfo[threadIdx.x] = ex | (cc << 16);
+  }
+  __syncthreads();
+  BASE_TICK(4);
+  uint32_t fs[ITEMS];  // fine bin | smem slot << 16
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    fs[j] = 0;
+    if (j * NT + threadIdx.x < len) {
+      fs[j] = base_fine_bin(v[j], sh, ss.cinfo);
+      atomicAdd(&fh[fs[j]], 1u);
+    }
+  }
+  __syncthreads();
+  BASE_TICK(5);
+  // exclusive scan of the NT*ITEMS fine-bin counts: thread t owns bins [ITEMS t, ITEMS t + ITEMS)
   uint32_t mxc = 0;
   {
-    const uint32_t b0 = threadIdx.x * kBaseItems;
-    uint32_t c[kBaseItems], sum = 0;
+    uint4* f4 = reinterpret_cast<uint4*>(fh) + threadIdx.x * (ITEMS / 4);
+    uint32_t sum = 0;
 #pragma unroll
-    for (int j = 0; j < kBaseItems; ++j) {
-      c[j] = (b0 + j < len) ? fh[b0 + j] : 0u;
-      sum += c[j];
-      mxc = max(mxc, c[j]);
+    for (int q = 0; q < ITEMS / 4; ++q) {
+      const uint4 c = f4[q];
+      sum += c.x + c.y + c.z + c.w;
+      mxc = max(mxc, max(max(c.x, c.y), max(c.z, c.w)));
     }
-    uint32_t run = block_exclusive_scan<kBaseThreads>(sum, ss.warp, nullptr);
+    uint32_t run = block_exclusive_scan<NT>(sum, ss.warp, nullptr);
 #pragma unroll
-    for (int j = 0; j < kBaseItems; ++j) {
-      if (b0 + j < len) fh[b0 + j] = run;
-      run += c[j];
+    for (int q = 0; q < ITEMS / 4; ++q) {
+      const uint4 c = f4[q];
+      uint4 o;
+      o.x = run; run += c.x;
+      o.y = run; run += c.y;
+      o.z = run; run += c.z;
+      o.w = run; run += c.w;
+      f4[q] = o;
     }
   }
   const bool overflow = __syncthreads_or(mxc > kFineOverflow) != 0;
+  BASE_TICK(6);
 #pragma unroll
-  for (int j = 0; j < kBaseItems; ++j) {
-    const uint32_t i = j * kBaseThreads + threadIdx.x;
-    if (i < len) tmp[atomicAdd(&fh[f[j]], 1u)] = v[j];
+  for (int j = 0; j < ITEMS; ++j) {
+    if (j * NT + threadIdx.x < len) {
+      const uint32_t slot = atomicAdd(&fh[fs[j]], 1u);
+      B[slot] = v[j];
+      fs[j] |= slot << 16;
+    }
   }
   __syncthreads();
-  if (!overflow) {
-    for (uint32_t b = threadIdx.x; b < len; b += kBaseThreads) {
-      const uint32_t beg = b ? fh[b - 1] : 0u, end = fh[b];
-      for (uint32_t i = beg + 1; i < end; ++i) {
-        const uint64_t x = tmp[i];
-        uint32_t j = i;
-        while (j > beg && tmp[j - 1] > x) { tmp[j] = tmp[j - 1]; --j; }
-        tmp[j] = x;
+  BASE_TICK(7);
+  if (overflow) {
+    bitonic_sort_smem<NT>(B, len);
+    return B;
+  }
+  // fh[f] is now the end of fine bin f.  Every key counts the keys of its bin that precede
+  // it (smaller, or equal at a smaller slot) and lands at bin start + that rank.
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    if (j * NT + threadIdx.x < len) {
+      const uint32_t f = fs[j] & 0xffffu, slot = fs[j] >> 16;
+      const uint32_t beg = f ? fh[f - 1] : 0u, end = fh[f];
+      const uint64_t d = v[j];
+      uint32_t r = beg;
+      for (uint32_t q = beg; q < end; ++q) {
+        const uint64_t y = B[q];
+        r += (y < d || (y == d && q < slot)) ? 1u : 0u;
+      }
+      B2[r] = d;
+    }
+  }
+  __syncthreads();
+  BASE_TICK(8);
+  return B2;
+}
+
+template <bool F64, bool NANCHK>
+__global__ __launch_bounds__(kPBThreads, 1) void k_base_sort(
+    const Window* __restrict__ wins, uint32_t nwin, uint32_t* __restrict__ ticket,
+    uint64_t* __restrict__ user, const uint64_t* __restrict__ scr, uint32_t* __restrict__ err) {
+  constexpr int NT = kPBThreads, ITEMS = kPBItems;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* A0 = reinterpret_cast<uint64_t*>(smraw);           // 2 x kPBStride (window buffers)
+  uint64_t* B2 = A0 + 2 * kPBStride;                            // kBaseMax
+  uint32_t* fh = reinterpret_cast<uint32_t*>(B2 + kBaseMax);    // kBaseMax
+  __shared__ BaseSmem ss;
+  long long t_prev_ = clock64();
+  uint64_t hk = 0, tk = 0;  // thread 0: head/tail keys of the window being prefetched
+  auto issue = [&](uint32_t w, int b) {  // thread 0: start the bulk copy of window w into buffer b
+    const Window wv = wins[w];
+    const uint64_t* g = (wv.buf ? scr : user) + wv.begin;
+    const WinGeom gm = win_geom(g, wv.len);
+    if (gm.body) {
+      mbar_arrive_tx(&ss.mbar[b], gm.body * 8u);
+      bulk_g2s(A0 + (size_t)b * kPBStride + 2, g + gm.head, gm.body * 8u, &ss.mbar[b]);
+    } else {
+      mbar_arrive(&ss.mbar[b]);
+    }
+    if (gm.head) hk = __ldcs(g);
+    if (gm.tail) tk = __ldcs(g + wv.len - 1);
+  };
+  auto place_ends = [&](uint32_t w, int b) {  // thread 0: store head/tail keys beside the body
+    const Window wv = wins[w];
+    const uint64_t* g = (wv.buf ? scr : user) + wv.begin;
+    const WinGeom gm = win_geom(g, wv.len);
+    uint64_t* A = A0 + (size_t)b * kPBStride;
+    if (gm.head) A[1] = hk;
+    if (gm.tail) A[2 + gm.body] = tk;
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&ss.mbar[0], 1);
+    mbar_init(&ss.mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t w = atomicAdd(ticket, 1u);
+    ss.win[0] = w;
+    if (w < nwin) { issue(w, 0); place_ends(w, 0); }
+  }
+  __syncthreads();
+  for (uint32_t it = 0;; ++it) {
+    const int b = it & 1;
+    const uint32_t cur = ss.win[b];
+    if (cur >= nwin) break;
+    uint32_t nxt = 0;
+    if (threadIdx.x == 0) {
+      nxt = atomicAdd(ticket, 1u);
+      ss.win[b ^ 1] = nxt;
+      if (nxt < nwin) issue(nxt, b ^ 1);
+    }
+    const Window wv = wins[cur];
+    const uint64_t* g = (wv.buf ? scr : user) + wv.begin;
+    uint64_t* dst = user + wv.begin;
+    const uint32_t len = wv.len;
+    const WinGeom gm = win_geom(g, len);
+    uint64_t* A = A0 + (size_t)b * kPBStride;
+    const uint64_t* K = A + 2 - gm.head;  // key i of the window
+  BASE_TICK(0);
+    mbar_wait(&ss.mbar[b], (it >> 1) & 1);
+  BASE_TICK(1);
+    uint64_t v[ITEMS];
+    bool nan_seen = false;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const uint32_t i = j * NT + threadIdx.x;
+      const uint64_t bits = (i < len) ? K[i] : 0ull;
+      if (F64 && NANCHK) nan_seen |= isnan(__longlong_as_double((long long)bits));
+      v[j] = ok_of<F64>(bits);
+    }
+    if (NANCHK) {
+      if (__syncthreads_or(nan_seen)) {
+        if (threadIdx.x == 0) atomicOr(err, kErrNan);
+        break;  // block-uniform; the array is left untouched
+      }
+    } else {
+      __syncthreads();  // A is free: it becomes the placement array
+    }
+    uint64_t mn;
+    const uint64_t* out = sort_regs_to_smem<NT, ITEMS>(v, len, A, B2, fh, ss, mn, t_prev_);
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const uint32_t i = j * NT + threadIdx.x;
+      if (i < len) __stcs(dst + i, bits_of_ok<F64>(out[i] + mn));
+    }
+  BASE_TICK(9);
+    if (threadIdx.x == 0 && nxt < nwin) place_ends(nxt, b ^ 1);
+    fence_proxy_async_smem();  // generic accesses to A before the next bulk copy into it
+    __syncthreads();
+  BASE_TICK(10);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Base case for small windows (<= kWBCap keys): persistent warps, one window per warp at a
+// time, no CTA barriers.  Each warp streams its next window into a second smem buffer with a
+// TMA bulk copy (mbarrier completion) while it sorts the current one, so every SM keeps
+// ~kWBWarps x 4 KB of loads in flight independently of the sorting work.  Windows are dealt
+// round-robin to the warps of the grid (a contended global ticket per window would
+// serialise at the L2).  Loops over the window are rolled (keys and per-key state live in
+// smem, not in unrolled register arrays) so the kernel stays small in the instruction cache.
+//
+// Sort = interpolation sort on the raw keys.  Bin of a key = trunc((x - min) * nb / (max -
+// min)) evaluated in binary64 (f64 keys directly, u64 keys through the exact difference
+// x - min converted to double): every step is monotone, so bins are ordered.  Counting pass
+// into smem, placement, then every key counts the keys of its bin that precede it in
+// ordering-key order (ties by slot) and lands at bin start + that count; the walk length is
+// the largest bin among the 32 lanes (warp-uniform).  Windows whose range is zero or not
+// finite (+-0.0 mixes, infinities, overflow) or whose bins overflow (> kFineOverflow keys:
+// extreme skew) take an exact warp bitonic sort.
+
+// strict "a sorts before b" by ordering key, on raw bits
+template <bool F64>
+__device__ __forceinline__ bool key_before(uint64_t a, uint64_t b) {
+  if constexpr (F64) {
+    const double da = __longlong_as_double((long long)a), db = __longlong_as_double((long long)b);
+    return da < db || (da == db && (long long)a < (long long)b);  // -0.0 before +0.0
+  } else {
+    return a < b;
+  }
+}
+
+// exact warp bitonic sort of B[0, len) by ordering key (B has room for the next power of 2)
+template <bool F64>
+__device__ void warp_bitonic_ok(uint64_t* B, uint32_t len, int lane) {
+  uint32_t NP = 32;
+  while (NP < len) NP <<= 1;
+  for (uint32_t i = len + lane; i < NP; i += 32) B[i] = ~0ull;  // ordering-key sentinel
+  for (uint32_t i = lane; i < len; i += 32) B[i] = ok_of<F64>(B[i]);
+  __syncwarp();
+  for (uint32_t size = 2; size <= NP; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t i = lane; i < NP / 2; i += 32) {
+        const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const uint64_t x = B[lo], y = B[hi];
+        if ((x > y) == asc) { B[lo] = y; B[hi] = x; }
+      }
+      __syncwarp();
+    }
+  }
+  for (uint32_t i = lane; i < len; i += 32) B[i] = bits_of_ok<F64>(B[i]);
+  __syncwarp();
+}
+
+template <bool F64>
+__global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
+    const Window* __restrict__ wins, uint32_t nwin, uint64_t* __restrict__ user,
+    const uint64_t* __restrict__ scr) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ uint64_t s_mbar[kWBWarps][2];
+  constexpr int BPL = kWBBins / 32;  // bins per lane
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  uint64_t* IN = reinterpret_cast<uint64_t*>(smraw + wp * kWBSmemPerWarp);  // 2 x kWBStride
+  uint64_t* B = IN + 2 * kWBStride;                                          // kWBCap
+  uint32_t* FS = reinterpret_cast<uint32_t*>(B + kWBCap);                    // kWBCap
+  uint32_t* bins = FS + kWBCap;                                              // kWBBins + 32
+  uint64_t* mbar = s_mbar[wp];
+  const uint32_t gw = blockIdx.x * kWBWarps + wp, gstride = gridDim.x * kWBWarps;
+  auto fetch = [&](uint32_t w, int b, Window& wv) {  // lane 0: bulk copy of window w -> IN[b]
+    if (lane == 0 && w < nwin) {
+      wv = wins[w];
+      const uint64_t* g = (wv.buf ? scr : user) + wv.begin;
+      const WinGeom gm = win_geom(g, wv.len);
+      if (gm.body) {
+        mbar_arrive_tx(&mbar[b], gm.body * 8u);
+        bulk_g2s(IN + (size_t)b * kWBStride + 2, g + gm.head, gm.body * 8u, &mbar[b]);
+      } else {
+        mbar_arrive(&mbar[b]);
       }
     }
-    __syncthreads();
-  } else {
-    bitonic_sort_smem<kBaseThreads>(tmp, len);
+  };
+  if (lane == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (uint32_t i = threadIdx.x; i < len; i += kBaseThreads) __stcs(dst + i, bits_of_ok<F64>(tmp[i]));
+  __syncwarp();
+  Window nwv{};
+  fetch(gw, 0, nwv);
+  for (uint32_t it = 0, cur = gw; cur < nwin; ++it, cur += gstride) {
+    const int b = it & 1;
+    Window wv;
+    wv.begin = __shfl_sync(0xffffffffu, nwv.begin, 0);
+    wv.len = __shfl_sync(0xffffffffu, nwv.len, 0);
+    wv.buf = __shfl_sync(0xffffffffu, nwv.buf, 0);
+    fetch(cur + gstride, b ^ 1, nwv);
+    const uint32_t len = wv.len;
+    const uint64_t* src = (wv.buf ? scr : user) + wv.begin;
+    uint64_t* dst = user + wv.begin;
+    const WinGeom gm = win_geom(src, len);
+    uint64_t* INb = IN + (size_t)b * kWBStride;
+    uint64_t* K = INb + 2 - gm.head;  // key i of the window
+    if (lane == 0 && gm.head) K[0] = __ldcs(src);
+    if (lane == 1 && gm.tail) K[len - 1] = __ldcs(src + len - 1);
+    mbar_wait(&mbar[b], (it >> 1) & 1);
+    __syncwarp();
+    // ---- bounds ----
+    double mn = 0.0, range;
+    uint64_t umn = ~0ull, umx = 0ull;
+    if constexpr (F64) {
+      double mx = -__longlong_as_double(0x7ff0000000000000ll);
+      mn = -mx;
+      for (uint32_t i = lane; i < len; i += 32) {
+        const double x = __longlong_as_double((long long)K[i]);
+        mn = fmin(mn, x);
+        mx = fmax(mx, x);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      range = mx - mn;
+    } else {
+      for (uint32_t i = lane; i < len; i += 32) {
+        const uint64_t x = K[i];
+        umn = min(umn, x);
+        umx = max(umx, x);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        umn = min(umn, __shfl_xor_sync(0xffffffffu, umn, o));
+        umx = max(umx, __shfl_xor_sync(0xffffffffu, umx, o));
+      }
+      range = (double)(umx - umn);
+    }
+    const uint64_t* OUT = K;  // constant (u64) windows are already sorted
+    if (!F64 && umn == umx) {
+      // nothing to sort
+    } else if (!(range > 0.0) || !(range < 1.79e308)) {  // +-0 mixes, infinities, overflow
+      for (uint32_t i = lane; i < len; i += 32) B[i] = K[i];
+      __syncwarp();
+      warp_bitonic_ok<F64>(B, len, lane);
+      OUT = B;
+    } else {
+      const uint32_t nb = kWBBinsPerKey * len;
+      const double scale = (double)nb / range;
+      // Bin f lives at bins[f + f / BPL] (one pad word per lane-owned group) so that the
+      // lane-contiguous scan walk is conflict-free.
+      for (uint32_t q = lane; q < (uint32_t)(kWBBins + 32); q += 32) bins[q] = 0u;
+      __syncwarp();
+      for (uint32_t i = lane; i < len; i += 32) {
+        const uint64_t x = K[i];
+        double y;
+        if constexpr (F64) y = __longlong_as_double((long long)x) - mn;
+        else y = (double)(x - umn);
+        uint32_t fb = min(__double2uint_rz(y * scale), nb - 1);
+        fb += fb / BPL;
+        FS[i] = fb;
+        atomicAdd(&bins[fb], 1u);
+      }
+      __syncwarp();
+      uint32_t mxc = 0;
+      {
+        uint32_t* bl0 = bins + lane * (BPL + 1);
+        uint32_t sum = 0;
+#pragma unroll 8
+        for (int q = 0; q < BPL; ++q) {
+          const uint32_t c = bl0[q];
+          sum += c;
+          mxc = max(mxc, c);
+        }
+        uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        uint32_t run = inc - sum;
+#pragma unroll 8
+        for (int q = 0; q < BPL; ++q) {
+          const uint32_t c = bl0[q];
+          bl0[q] = run;
+          run += c;
+        }
+      }
+      const bool overflow = __any_sync(0xffffffffu, mxc > kFineOverflow);
+      __syncwarp();
+      for (uint32_t i = lane; i < len; i += 32) {
+        const uint32_t fb = FS[i];
+        const uint32_t slot = atomicAdd(&bins[fb], 1u);
+        B[slot] = K[i];
+        FS[i] = fb | (slot << 16);
+      }
+      __syncwarp();
+      if (overflow) {
+        warp_bitonic_ok<F64>(B, len, lane);
+        OUT = B;
+      } else {
+        // bins hold bin ends now; every key ranks itself among its bin and lands in INb
+        // (the input copy is dead: keys are read back from B).
+        for (uint32_t base = 0; base < len; base += 32) {
+          const uint32_t i = base + lane;
+          const bool valid = i < len;
+          uint32_t fb = 0, slot = 0, beg = 0, end = 0;
+          uint64_t x = 0;
+          if (valid) {
+            const uint32_t w = FS[i];
+            fb = w & 0xffffu;
+            slot = w >> 16;
+            beg = (fb % (BPL + 1)) ? bins[fb - 1] : (fb ? bins[fb - 2] : 0u);
+            end = bins[fb];
+            x = B[slot];
+          }
+          const uint32_t n = __reduce_max_sync(0xffffffffu, end - beg);
+          uint32_t r = beg;
+          for (uint32_t q = 1; q < n; ++q) {  // n == 1: every key is alone in its bin
+            const uint32_t p0 = beg + q - 1;
+            const uint32_t p = p0 < slot ? p0 : p0 + 1;  // skip the key's own slot
+            if (p < end) {
+              const uint64_t y = B[p];
+              r += (key_before<F64>(y, x) || (y == x && p < slot)) ? 1u : 0u;
+            }
+          }
+          if (valid) INb[r] = x;
+        }
+        OUT = INb;
+      }
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < len; i += 32) __stcs(dst + i, OUT[i]);
+    fence_proxy_async_smem();  // generic accesses to IN[b] before the bulk copy that reuses it
+    __syncwarp();
+  }
 }
 
 __global__ void k_fill(const Fill* __restrict__ fills, uint64_t* __restrict__ user) {
