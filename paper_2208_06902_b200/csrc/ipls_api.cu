@@ -173,7 +173,7 @@ FixedLayout fixed_layout(const Params& p) {
 // Per-level metadata (sized by the level's actual counts).  `status` comes first so a fresh
 // allocation can be cleared cheaply.
 struct MetaLayout {
-  size_t status, cnt_agg, rep_agg, chunk_pre, models, samples, seg_dst, seg_tot, total;
+  size_t status, cflag, cref, chunk_pre, models, samples, seg_dst, seg_tot, seg_done, total;
 };
 
 MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_t k) {
@@ -181,13 +181,14 @@ MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
   L.status = take(chunks * k * 8);
-  L.cnt_agg = take(chunks * k * 4);
-  L.rep_agg = take(chunks * k * 8);
+  L.cflag = take(chunks * k);
+  L.cref = take(chunks * k * 8);
   L.chunk_pre = take(chunks * k * 4);
   L.models = take(segs * sizeof(ModelDev));
   L.samples = take(samples * 8 + 64);
   L.seg_dst = take(segs * k * 8);
   L.seg_tot = take(segs * k * 4);
+  L.seg_done = take(segs * 4);
   L.total = o;
   return L;
 }
@@ -253,21 +254,13 @@ struct TraceSink {
   std::vector<std::vector<uint64_t>> counts, samples;
 };
 
-size_t scatter_smem(uint32_t k) {
-  return (size_t)kSTile * 8 + (size_t)k * 8 + (size_t)k * kPendSlots * 8 + (size_t)kSTile * 4 +
-         (size_t)(kSWarps / 2) * k * 4 + (size_t)(k + 1) * 4 + (size_t)k * 8 + (size_t)k;
-}
 template <bool F64>
-void launch_scatter(uint32_t nchunk, cudaStream_t st, const uint64_t* src, uint64_t* user,
-                    uint64_t* scr, const ChunkDesc* chunks, const ModelDev* models, uint32_t k,
-                    const uint32_t* chunk_pre, const uint64_t* seg_dst, const uint32_t* err) {
-  k_scatter<F64><<<nchunk, kSThreads, scatter_smem(k), st>>>(src, user, scr, chunks, models, k,
-                                                             chunk_pre, seg_dst, err);
+void launch_scatter(uint32_t nchunk, cudaStream_t st, const LevelArgs& la, uint64_t* user,
+                    uint64_t* scr) {
+  k_scatter<F64><<<nchunk, kSThreads4, scatter_smem_bytes(la.k), st>>>(la, user, scr);
   ck_launch();
 }
-size_t classify_smem(uint32_t k) {
-  return std::max((size_t)k * 8 + (size_t)k * 12, win_scratch_bytes(k));
-}
+size_t classify_smem(uint32_t k) { return (size_t)k * 4; }
 size_t warp_base_smem() { return kWBSmemPerWarp * kWBWarps; }
 size_t base_smem() { return (size_t)2 * kPBStride * 8 + (size_t)kBaseMax * 12; }
 int g_num_sms = 0;
@@ -301,7 +294,7 @@ void set_attrs() {
   ck(cudaFuncSetAttribute(k_classify_scan<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)classify_smem(kMaxK)));
   ck(cudaFuncSetAttribute(k_scatter<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)scatter_smem(kMaxK)));
+                          (int)std::max(scatter_smem_bytes(kMaxK), win_scratch_bytes(kMaxK))));
 
   done = true;
 }
@@ -393,6 +386,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     uint32_t* chunk_pre = at<uint32_t>(meta, ML.chunk_pre);
 
     ck(cudaMemsetAsync(nctr, 0, sizeof(LevelCounters), st));
+    ck(cudaMemsetAsync(at<uint32_t>(meta, ML.seg_done), 0, (size_t)nseg * 4, st));
     {
       IPLS_PROF("gather_fit", 0);
       const uint32_t cap = fit_cap(max_S);
@@ -405,11 +399,12 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     la.k = k; la.base_case = p.B; la.level = level; la.chunk_keys = p.chunk_keys;
     la.ticket = &cctr->ticket;
     la.status = at<uint64_t>(meta, ML.status);
-    la.cnt_agg = at<uint32_t>(meta, ML.cnt_agg);
-    la.rep_agg = at<uint64_t>(meta, ML.rep_agg);
+    la.cflag = at<uint8_t>(meta, ML.cflag);
+    la.cref = at<uint64_t>(meta, ML.cref);
+    la.seg_done = at<uint32_t>(meta, ML.seg_done);
     la.chunk_pre = chunk_pre;
     la.seg_dst = seg_dst;
-    la.seg_tot = trace ? seg_tot : nullptr;
+    la.seg_tot = seg_tot;
     la.epoch = epoch;
     la.err = d_err;
     la.check_nan = (F64 && level == 0) ? 1 : 0;
@@ -428,8 +423,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     }
     {
       IPLS_PROF("scatter", 16.0 * level_keys);
-      launch_scatter<F64>(nchunk, st, src, keys, scr, chunks, models, k, chunk_pre, seg_dst,
-                          d_err);
+      launch_scatter<F64>(nchunk, st, la, keys, scr);
     }
 
     if (trace) {
@@ -741,11 +735,12 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
     la.models = dmod; la.k = k; la.base_case = 0; la.level = 0; la.chunk_keys = ck_keys;
     la.ticket = &dctr->ticket;
     la.status = at<uint64_t>(meta, ML.status);
-    la.cnt_agg = at<uint32_t>(meta, ML.cnt_agg);
-    la.rep_agg = at<uint64_t>(meta, ML.rep_agg);
+    la.cflag = at<uint8_t>(meta, ML.cflag);
+    la.cref = at<uint64_t>(meta, ML.cref);
+    la.seg_done = at<uint32_t>(meta, ML.seg_done);
     la.chunk_pre = at<uint32_t>(meta, ML.chunk_pre);
     la.seg_dst = at<uint64_t>(meta, ML.seg_dst);
-    la.seg_tot = nullptr;
+    la.seg_tot = at<uint32_t>(meta, ML.seg_tot);
     bool wrapped = false;
     la.epoch = next_epoch(&wrapped);
     la.err = derr;
@@ -758,8 +753,7 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
       set_attrs<F64>();
       k_classify_scan<F64><<<nchunk, kCThreads, classify_smem(k), st>>>(la);
       ck_launch();
-      launch_scatter<F64>(nchunk, st, la.src, out, out, dch, dmod, k, la.chunk_pre, la.seg_dst,
-                          derr);
+      launch_scatter<F64>(nchunk, st, la, out, out);
     };
     if (t == IPLS_KEY_F64) body(std::true_type{}); else body(std::false_type{});
     ck(cudaStreamSynchronize(st));

@@ -18,10 +18,6 @@ namespace ipls {
 constexpr int kCThreads = 512;                 // classify
 constexpr int kCItems = 8;
 constexpr int kCTile = kCThreads * kCItems;    // 4096
-constexpr int kSThreads = 256;                 // scatter
-constexpr int kSWarps = kSThreads / 32;        // 8
-constexpr int kSRounds = 16;  // keys per thread per tile
-constexpr int kSTile = kSThreads * kSRounds;   // 4096
 constexpr int kFitThreads = 1024;
 constexpr int kFitMaxS = 8192;
 constexpr int kBaseMax = 8192;                 // keys per base-case window (W + B)
@@ -298,12 +294,13 @@ struct LevelArgs {
   const ModelDev* models;
   uint32_t k, base_case, level, chunk_keys;
   uint32_t* ticket;
-  uint64_t* status;      // [chunk][k]: epoch<<48 | state<<46 | inh<<45 | count
-  uint32_t* cnt_agg;     // [chunk][k]: own count | inh<<31
-  uint64_t* rep_agg;     // [chunk][k]: own representative key
+  uint64_t* status;      // [chunk][k]: epoch<<48 | state<<46 | count
   uint32_t* chunk_pre;   // [chunk][k] exclusive prefix within the segment
   uint64_t* seg_dst;     // [seg][k]   encoded destination base of every child
-  uint32_t* seg_tot;     // [seg][k]   child counts (trace)
+  uint32_t* seg_tot;     // [seg][k]   child counts
+  uint8_t* cflag;        // [chunk][k] scatter homogeneity flag: 0 empty, 1 one value, 2 several
+  uint64_t* cref;        // [chunk][k] the chunk's value of a one-value bucket
+  uint32_t* seg_done;    // [seg]      chunks of the segment scattered so far
   uint32_t epoch;
   uint32_t* err;
   int check_nan;
@@ -471,15 +468,69 @@ __device__ void pack_windows(const LevelArgs& a, const SegDesc& sg, uint32_t k,
   __syncthreads();  // scratch is reused by the next packing
 }
 
-__device__ void segment_offsets(const LevelArgs& a, uint32_t s, const SegDesc& sg,
-                                const ModelDev& md, const uint32_t (&tot)[kCBpt],
-                                const uint32_t (&inh)[kCBpt], const uint64_t (&rep)[kCBpt],
-                                OffSmem& os, uint32_t* wsm) {
+// Per segment, at the end of phase 4a (run by the CTA that finished the segment's last
+// chunk): bucket bases (exclusive scan over k) and child counts.  Thread t owns buckets
+// 2t, 2t+1.
+__device__ void segment_bases(const LevelArgs& a, uint32_t s, const SegDesc& sg,
+                              const ModelDev& md, const uint32_t (&tot)[kCBpt], OffSmem& os) {
   const uint32_t k = a.k;
-  uint32_t bb[kCBpt], base[kCBpt];
   uint32_t x = 0;
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) { bb[q] = threadIdx.x * kCBpt + q; x += tot[q]; }
+  for (int q = 0; q < kCBpt; ++q) x += tot[q];
+  uint32_t ex = block_exclusive_scan<kCThreads>(x, os.warp, nullptr);
+  const uint32_t dstbuf = (a.level + 1) & 1;  // 1 = scratch, 0 = user array
+#pragma unroll
+  for (int q = 0; q < kCBpt; ++q) {
+    const uint32_t b = threadIdx.x * kCBpt + q;
+    if (b < k) {
+      const uint64_t enc = a.single_offsets ? (uint64_t)ex
+                                            : ((dstbuf == 0 ? kDstUserBit : 0ull) | (sg.begin + ex));
+      a.seg_dst[(size_t)s * k + b] = enc;
+      a.seg_tot[(size_t)s * k + b] = tot[q];
+      if (a.single_offsets && b < md.k_eff) a.single_offsets[b] = ex;
+    }
+    ex += tot[q];
+  }
+  if (a.single_offsets && threadIdx.x == 0) a.single_offsets[md.k_eff] = sg.m;
+}
+
+// Per segment, after its last chunk has been scattered (run by that CTA): child classes with
+// the precedence of R20 (homogeneous > base > partition; small homogeneous children go with
+// the base case, which leaves them unchanged), the no-progress guard (R10), next-level work,
+// base-case windows and fills.  Homogeneity of a child (R9) is merged here from
+// the per-(chunk, bucket) flags the scatter recorded: a child is homogeneous iff every chunk
+// that holds keys of it saw one value and all those values agree.  Only children above the
+// base case can be classed homogeneous-final, so only they are merged.
+__device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, const ModelDev& md,
+                             OffSmem& os, uint32_t* wsm) {
+  const uint32_t k = a.k;
+  uint32_t bb[kCBpt], base[kCBpt], tot[kCBpt], inh[kCBpt];
+  uint64_t rep[kCBpt];
+  uint32_t x = 0;
+#pragma unroll
+  for (int q = 0; q < kCBpt; ++q) {
+    bb[q] = threadIdx.x * kCBpt + q;
+    tot[q] = (bb[q] < k) ? a.seg_tot[(size_t)s * k + bb[q]] : 0u;
+    x += tot[q];
+    inh[q] = 1;
+    rep[q] = 0;
+    if (bb[q] < k && tot[q] > a.base_case) {
+      bool have = false;
+      uint64_t ref = 0;
+      inh[q] = 0;
+      for (uint32_t j = sg.chunk_first; j < sg.chunk_first + sg.nchunks; ++j) {
+        const size_t jx = (size_t)j * k + bb[q];
+        const uint8_t f = a.cflag[jx];
+        if (f == 0) continue;
+        if (f == 2) { inh[q] = 1; break; }
+        const uint64_t r = a.cref[jx];
+        if (have && r != ref) { inh[q] = 1; break; }
+        ref = r;
+        have = true;
+      }
+      rep[q] = ref;
+    }
+  }
   uint32_t ex = block_exclusive_scan<kCThreads>(x, os.warp, nullptr);
 #pragma unroll
   for (int q = 0; q < kCBpt; ++q) { base[q] = ex; ex += tot[q]; }
@@ -489,28 +540,12 @@ __device__ void segment_offsets(const LevelArgs& a, uint32_t s, const SegDesc& s
     if (md.kind == kModelLinear && bb[q] < k && tot[q] == sg.m) st = 1;
   const bool stuck = __syncthreads_or(st) != 0;
   const uint32_t dstbuf = (a.level + 1) & 1;  // 1 = scratch, 0 = user array
-#pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
-    if (bb[q] < k) {
-      uint64_t enc = a.single_offsets ? (uint64_t)base[q]
-                                      : ((dstbuf == 0 ? kDstUserBit : 0ull) | (sg.begin + base[q]));
-      a.seg_dst[(size_t)s * k + bb[q]] = enc;
-      if (a.seg_tot) a.seg_tot[(size_t)s * k + bb[q]] = tot[q];
-    }
-  }
-  if (a.single_offsets) {
-#pragma unroll
-    for (int q = 0; q < kCBpt; ++q)
-      if (bb[q] < md.k_eff) a.single_offsets[bb[q]] = base[q];
-    if (threadIdx.x == 0) a.single_offsets[md.k_eff] = sg.m;
-    return;
-  }
   uint32_t cls[kCBpt];
 #pragma unroll
   for (int q = 0; q < kCBpt; ++q) {
     cls[q] = 0;  // 0 empty, 1 base (or small homogeneous), 2 partition, 3 big homogeneous
     if (!stuck && bb[q] < k && tot[q] > 0) {
-      bool homog = (md.kind == kModelEq3 && bb[q] == 1) || !inh[q];
+      const bool homog = (md.kind == kModelEq3 && bb[q] == 1) || !inh[q];
       if (tot[q] <= a.base_case) cls[q] = 1;
       else if (homog) cls[q] = 3;
       else cls[q] = 2;
@@ -602,13 +637,12 @@ __device__ void segment_offsets(const LevelArgs& a, uint32_t s, const SegDesc& s
 }
 
 // Tile loop of phase 4a with the model kind and the optional outputs fixed at compile time.
-// Per key: model evaluation (2 RN ops + saturating convert), one smem atomicAdd into the
-// chunk histogram, and the homogeneity representative (racy store; after a barrier every
-// key compares against it).  The next tile is loaded while this one is classified.
+// Per key: model evaluation (2 RN ops + saturating convert) and one smem atomicAdd into the
+// chunk histogram (+ the NaN test at level 0).  The next tile is loaded while this one is
+// classified.
 template <bool F64, bool EQ3, bool NANCHK, bool IDS>
 __device__ void classify_tiles(const LevelArgs& a, const ChunkDesc& ch, const ModelDev& md,
-                               uint32_t* hist, uint64_t* rep, uint32_t* has, uint32_t* inhs,
-                               int& nan_seen) {
+                               uint32_t* hist, int& nan_seen) {
   const Bucketer<F64, EQ3> bucket(md, a.k);
   const uint64_t* p = a.src + ch.start;
   uint64_t cur[kCItems], nxt[kCItems];
@@ -617,6 +651,7 @@ __device__ void classify_tiles(const LevelArgs& a, const ChunkDesc& ch, const Mo
     const uint32_t i = r * kCThreads + threadIdx.x;
     cur[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
   }
+  bool nan = false;
   for (uint32_t t0 = 0; t0 < ch.len; t0 += kCTile) {
     const uint32_t tl = min((uint32_t)kCTile, ch.len - t0);
     const uint32_t t1 = t0 + kCTile;
@@ -625,58 +660,43 @@ __device__ void classify_tiles(const LevelArgs& a, const ChunkDesc& ch, const Mo
       const uint32_t i = t1 + r * kCThreads + threadIdx.x;
       nxt[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
     }
-    uint32_t bk[kCItems];
 #pragma unroll
     for (int r = 0; r < kCItems; ++r) {
       const uint32_t i = r * kCThreads + threadIdx.x;
       if (i < tl) {
-        if (NANCHK && is_nan_bits(cur[r])) nan_seen = 1;
-        bk[r] = bucket(cur[r]);
-        atomicAdd(&hist[bk[r]], 1u);
-        if (!has[bk[r]]) rep[bk[r]] = cur[r];
-        if (IDS) a.ids[ch.start + t0 + i] = (uint16_t)bk[r];
+        if (NANCHK) nan |= isnan(__longlong_as_double((long long)cur[r]));
+        const uint32_t b = bucket(cur[r]);
+        atomicAdd(&hist[b], 1u);
+        if (IDS) a.ids[ch.start + t0 + i] = (uint16_t)b;
       }
     }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kCItems; ++r) {
-      const uint32_t i = r * kCThreads + threadIdx.x;
-      if (i < tl) {
-        has[bk[r]] = 1;
-        if (rep[bk[r]] != cur[r]) inhs[bk[r]] = 1;
-      }
-    }
-    __syncthreads();
 #pragma unroll
     for (int r = 0; r < kCItems; ++r) cur[r] = nxt[r];
   }
+  nan_seen = nan ? 1 : 0;
 }
 
 template <bool F64, bool EQ3>
 __device__ __forceinline__ void classify_dispatch(const LevelArgs& a, const ChunkDesc& ch,
                                                   const ModelDev& md, uint32_t* hist,
-                                                  uint64_t* rep, uint32_t* has, uint32_t* inhs,
                                                   int& nan_seen) {
   if (a.ids)
-    classify_tiles<F64, EQ3, false, true>(a, ch, md, hist, rep, has, inhs, nan_seen);
+    classify_tiles<F64, EQ3, false, true>(a, ch, md, hist, nan_seen);
   else if (F64 && a.check_nan)
-    classify_tiles<F64, EQ3, F64, false>(a, ch, md, hist, rep, has, inhs, nan_seen);
+    classify_tiles<F64, EQ3, F64, false>(a, ch, md, hist, nan_seen);
   else
-    classify_tiles<F64, EQ3, false, false>(a, ch, md, hist, rep, has, inhs, nan_seen);
+    classify_tiles<F64, EQ3, false, false>(a, ch, md, hist, nan_seen);
 }
 
 template <bool F64>
 __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const uint32_t k = a.k;
-  uint64_t* rep = reinterpret_cast<uint64_t*>(smraw);  // k
-  uint32_t* hist = reinterpret_cast<uint32_t*>(rep + k);
-  uint32_t* has = hist + k;
-  uint32_t* inhs = has + k;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smraw);  // k
   __shared__ uint32_t s_c;
   __shared__ OffSmem os;
   if (threadIdx.x == 0) s_c = atomicAdd(a.ticket, 1u);
-  for (uint32_t b = threadIdx.x; b < k; b += kCThreads) { hist[b] = 0; has[b] = 0; inhs[b] = 0; }
+  for (uint32_t b = threadIdx.x; b < k; b += kCThreads) hist[b] = 0;
   __syncthreads();
   const uint32_t c = s_c;
   const ChunkDesc ch = a.chunks[c];
@@ -684,45 +704,33 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
   const ModelDev md = a.models[ch.seg];
   int nan_seen = 0;
   if (md.kind == kModelEq3)
-    classify_dispatch<F64, true>(a, ch, md, hist, rep, has, inhs, nan_seen);
+    classify_dispatch<F64, true>(a, ch, md, hist, nan_seen);
   else
-    classify_dispatch<F64, false>(a, ch, md, hist, rep, has, inhs, nan_seen);
+    classify_dispatch<F64, false>(a, ch, md, hist, nan_seen);
   if (a.check_nan) {
     if (__syncthreads_or(nan_seen) && threadIdx.x == 0) atomicOr(a.err, kErrNan);
+  } else {
+    __syncthreads();
   }
   // ---- decoupled lookback over the chunks of this segment, bucket by bucket ----
-  // Every chunk first records its own count and representative (read only by the last
-  // chunk's homogeneity check), fences once, then publishes one 64-bit status word per
-  // bucket: AGG (own count) or INC (inclusive prefix), tagged with the level's epoch.
+  // One 64-bit status word per (chunk, bucket): AGG (own count) or INC (inclusive prefix),
+  // tagged with the level's epoch, so the status array needs no clearing between levels.
   const bool first = (c == sg.chunk_first);
   const bool last = (c == sg.chunk_first + sg.nchunks - 1);
-  uint32_t tot[kCBpt], inh[kCBpt];
-  uint64_t rp[kCBpt];
+  uint32_t tot[kCBpt];
 #pragma unroll
   for (int q = 0; q < kCBpt; ++q) {
     const uint32_t b = threadIdx.x * kCBpt + q;
-    tot[q] = hist[b < k ? b : 0]; inh[q] = inhs[b < k ? b : 0]; rp[q] = rep[b < k ? b : 0];
-    if (b < k && sg.nchunks > 1) {
-      const size_t ix = (size_t)c * k + b;
-      a.cnt_agg[ix] = tot[q] | (inh[q] << 31);
-      a.rep_agg[ix] = rp[q];
-    }
-  }
-  if (sg.nchunks > 1) {
-    __threadfence();
-#pragma unroll
-    for (int q = 0; q < kCBpt; ++q) {
-      const uint32_t b = threadIdx.x * kCBpt + q;
-      if (b < k && !last)
-        *((volatile uint64_t*)&a.status[(size_t)c * k + b]) =
-            pack_status(a.epoch, first ? kStInc : kStAgg, inh[q], tot[q]);
-    }
+    tot[q] = (b < k) ? hist[b] : 0u;
+    if (b < k && sg.nchunks > 1 && !last)
+      *((volatile uint64_t*)&a.status[(size_t)c * k + b]) =
+          pack_status(a.epoch, first ? kStInc : kStAgg, 0u, tot[q]);
   }
 #pragma unroll
   for (int q = 0; q < kCBpt; ++q) {
     const uint32_t b = threadIdx.x * kCBpt + q;
     if (b >= k) continue;
-    uint32_t ex_cnt = 0, ex_inh = 0;
+    uint32_t ex_cnt = 0;
     if (!first) {
       uint32_t j = c - 1;
       while (true) {
@@ -730,55 +738,23 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
         const uint32_t state = (uint32_t)(st >> 46) & 3u;
         if ((uint32_t)(st >> 48) != (a.epoch & 0xffff) || state == 0) continue;  // not yet
         ex_cnt += (uint32_t)st;
-        ex_inh |= (uint32_t)(st >> 45) & 1u;
         if (state == kStInc) break;
         --j;
       }
       if (!last)
         *((volatile uint64_t*)&a.status[(size_t)c * k + b]) =
-            pack_status(a.epoch, kStInc, inh[q] | ex_inh, ex_cnt + tot[q]);
+            pack_status(a.epoch, kStInc, 0u, ex_cnt + tot[q]);
     }
     a.chunk_pre[(size_t)c * k + b] = ex_cnt;
     tot[q] += ex_cnt;
-    inh[q] |= ex_inh;
   }
-  if (last && sg.nchunks > 1) {
-    // Homogeneity across chunks (R9): a child stays homogeneous only if every chunk that
-    // holds keys of it saw one value and all those values agree.  Only children that could
-    // be partitioned (> base case) matter (R20), so only they are checked.
-    __threadfence();
-#pragma unroll
-    for (int q = 0; q < kCBpt; ++q) {
-      const uint32_t b = threadIdx.x * kCBpt + q;
-      if (b >= k || inh[q] || tot[q] <= a.base_case) continue;
-      bool have = false;
-      uint64_t ref = 0;
-      for (uint32_t j = sg.chunk_first; j < c && !inh[q]; ++j) {
-        const size_t jx = (size_t)j * k + b;
-        const uint32_t cw = *((volatile const uint32_t*)&a.cnt_agg[jx]);
-        if ((cw & ~kInhBit) == 0) continue;
-        const uint64_t r = *((volatile const uint64_t*)&a.rep_agg[jx]);
-        if (cw & kInhBit) inh[q] = 1;
-        if (have && r != ref) inh[q] = 1;
-        if (!have) { ref = r; have = true; }
-      }
-      if (hist[b]) {
-        if (have && rep[b] != ref) inh[q] = 1;
-        if (!have) ref = rep[b];
-      }
-      rp[q] = ref;
-    }
-  }
-  if (last) {
-    __syncthreads();  // the histogram smem becomes window-formation scratch
-    segment_offsets(a, ch.seg, sg, md, tot, inh, rp, os, reinterpret_cast<uint32_t*>(smraw));
-  }
+  if (last) segment_bases(a, ch.seg, sg, md, tot, os);
 }
 
 // ------------------------------------------------------------------------------------
-// Phase 4b: stable scatter of one chunk (R11).
+// Phase 4b: stable scatter of one chunk (R11), 512 threads, 2 CTAs per SM.
 //
-// Tile = 4096 keys; warp w owns keys [512w, 512w+512) in 16 rounds of 32.
+// Tile = 4096 keys; warp w owns keys [256w, 256w+256) in 8 rounds of 32.
 // Rank: every key does one smem atomicAdd on its warp's counter for its bucket (u16 halves
 // of packed u32 words, two warps per word).  Same-address lanes of one atomic instruction
 // are served in lane order on B200 (tools/micro/atom_order.cu: 0 violations in 2.2e9 lane
@@ -787,154 +763,133 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
 // staged tile (tile index must increase inside every bucket run) while it is written out,
 // and any offending run is rewritten in index order afterwards, so the layout is stable by
 // construction whatever the hardware does.
-// Write-out: per bucket, a byte-address base and a flush limit are precomputed once per
-// tile, so a key costs one load of its (bucket, index) word, two smem loads and one store.
-// Only whole 32-byte sectors are written while a chunk is in flight: the 0-3 trailing keys
-// of a bucket that do not complete a sector wait in smem for the next tile (flushed at the
-// chunk's end).  Partial-sector writes cost an ECC read-modify-write fill in HBM (ncu:
-// lts__d_sectors_fill_device), which this avoids except at chunk boundaries.
-constexpr uint32_t kPendSlots = 3;
+// Write-out: key q of the staged tile goes to run_address[bucket] + 8 (q - tile_offset[bucket]);
+// a warp's 32 consecutive staged keys cover a few runs, so stores coalesce per run and the
+// L2 completes sectors shared by consecutive tiles before they are written back.
+// Homogeneity (R9): every key is compared with the first key of its bucket in the tile; the
+// per-bucket pass after the write-out compares that key with the chunk's first key of the
+// bucket.  The chunk's flags (0 empty, 1 one value, 2 several) and values go to global memory
+// for segment_emit.
+constexpr int kSThreads4 = 512;
+constexpr int kSWarps4 = kSThreads4 / 32;          // 16
+constexpr int kSRounds4 = 8;                       // keys per thread per tile
+constexpr int kSTile4 = kSThreads4 * kSRounds4;    // 4096
+constexpr int kSPairs4 = kSWarps4 / 2;             // warp pairs sharing a counter word
+
+__host__ __device__ constexpr size_t scatter_smem_bytes(uint32_t k) {
+  return (size_t)kSTile4 * 8 + (size_t)k * 8 + (size_t)k * 8 + (size_t)kSTile4 * 4 +
+         (size_t)kSPairs4 * k * 4 + (size_t)(k + 1) * 4 + (size_t)k + 16;
+}
 
 template <bool F64, bool EQ3>
-__device__ void scatter_tiles(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst_user,
-                              uint64_t* __restrict__ dst_scr, const ChunkDesc& ch,
-                              const ModelDev& md, uint32_t k, const uint32_t* __restrict__ chunk_pre,
-                              const uint64_t* __restrict__ seg_dst, unsigned char* smraw) {
-  uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);                  // kSTile
-  uint64_t* abase = stage + kSTile;                                      // k: byte address state
-  uint64_t* pend = abase + k;                                            // k * kPendSlots
-  uint32_t* sbi = reinterpret_cast<uint32_t*>(pend + (size_t)k * kPendSlots);  // kSTile
-  uint32_t* wc = sbi + kSTile;                                           // (kSWarps/2) * k
-  uint32_t* toff = wc + (kSWarps / 2) * k;                               // k + 1
-  int32_t* qlim = reinterpret_cast<int32_t*>(toff + k + 1);              // k
-  int32_t* pbase = qlim + k;                                             // k
-  uint8_t* plen = reinterpret_cast<uint8_t*>(pbase + k);                 // k
+__device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_user,
+                              uint64_t* __restrict__ dst_scr, uint32_t c, const ChunkDesc& ch,
+                              const ModelDev& md, unsigned char* smraw) {
+  constexpr int NT = kSThreads4;
+  const uint32_t k = a.k;
+  uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);         // kSTile4
+  uint64_t* runa = stage + kSTile4;                              // k: byte address of next write
+  uint64_t* ref = runa + k;                                      // k: chunk's first key
+  uint32_t* sbi = reinterpret_cast<uint32_t*>(ref + k);          // kSTile4: bucket << 16 | index
+  uint32_t* wc = sbi + kSTile4;                                  // kSPairs4 * k
+  uint32_t* toff = wc + kSPairs4 * k;                            // k + 1
+  uint8_t* cflag = reinterpret_cast<uint8_t*>(toff + k + 1);     // k
   __shared__ uint32_t s_warp[40];
-
   const Bucketer<F64, EQ3> bucket(md, k);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  // abase holds the byte address of the bucket's next destination between tiles
-  for (uint32_t b = threadIdx.x; b < k; b += kSThreads) {
-    const uint64_t d = seg_dst[(size_t)ch.seg * k + b] + chunk_pre[(size_t)blockIdx.x * k + b];
+  for (uint32_t b = threadIdx.x; b < k; b += NT) {
+    const uint64_t d = a.seg_dst[(size_t)ch.seg * k + b] + a.chunk_pre[(size_t)c * k + b];
     uint64_t* buf = (d & kDstUserBit) ? dst_user : dst_scr;
-    abase[b] = reinterpret_cast<uint64_t>(buf + (d & ~kDstUserBit));
-    plen[b] = 0;
+    runa[b] = reinterpret_cast<uint64_t>(buf + (d & ~kDstUserBit));
+    cflag[b] = 0;
   }
   uint32_t* wcw = wc + (wp >> 1) * k;
   const uint32_t winc = 1u << (16 * (wp & 1));
   const int wsh = 16 * (wp & 1);
-  const uint64_t* p = src + ch.start;
-  uint64_t key[kSRounds];
+  const uint64_t* p = a.src + ch.start;
+  uint64_t key[kSRounds4];
 #pragma unroll
-  for (int r = 0; r < kSRounds; ++r) {
-    const uint32_t i = wp * (kSRounds * 32) + r * 32 + lane;
+  for (int r = 0; r < kSRounds4; ++r) {
+    const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
     key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
   }
-  for (uint32_t t0 = 0; t0 < ch.len; t0 += kSTile) {
-    const uint32_t tl = min((uint32_t)kSTile, ch.len - t0);
-    const bool last_tile = t0 + kSTile >= ch.len;
-    for (uint32_t i = threadIdx.x; i < (kSWarps / 2) * k; i += kSThreads) wc[i] = 0u;
-    __syncthreads();
-    uint32_t bk[kSRounds], loc[kSRounds];
-#pragma unroll
-    for (int r = 0; r < kSRounds; ++r) {
-      const uint32_t i = wp * (kSRounds * 32) + r * 32 + lane;
-      bk[r] = (i < tl) ? bucket(key[r]) : 0u;
-    }
-#pragma unroll
-    for (int r = 0; r < kSRounds; ++r) {
-      const uint32_t i = wp * (kSRounds * 32) + r * 32 + lane;
-      loc[r] = (i < tl) ? ((atomicAdd(&wcw[bk[r]], winc) >> wsh) & 0xffffu) : 0u;
-    }
-    __syncthreads();
-    // cross-warp exclusive scan per bucket (warp order = key order); tile totals into toff
-    for (uint32_t b = threadIdx.x; b < k; b += kSThreads) {
-      uint32_t run = 0;
-#pragma unroll
-      for (int w2 = 0; w2 < kSWarps / 2; ++w2) {
-        const uint32_t wv = wc[w2 * k + b];
-        const uint32_t lo = wv & 0xffffu, hi = wv >> 16;
-        wc[w2 * k + b] = run | ((run + lo) << 16);
-        run += lo + hi;
-      }
-      toff[b] = run;
-    }
-    __syncthreads();
+  for (uint32_t t0 = 0; t0 < ch.len; t0 += kSTile4) {
+    const uint32_t tl = min((uint32_t)kSTile4, ch.len - t0);
     {
-      uint32_t c4[4], s4 = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t b = threadIdx.x * 4 + q;
-        c4[q] = (b < k) ? toff[b] : 0u;
-        s4 += c4[q];
-      }
-      uint32_t tot;
-      uint32_t ex = block_exclusive_scan<kSThreads>(s4, s_warp, &tot);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t b = threadIdx.x * 4 + q;
-        if (b < k) toff[b] = ex;
-        ex += c4[q];
-      }
-      if (threadIdx.x == 0) toff[k] = tot;
+      uint4* w4 = reinterpret_cast<uint4*>(wc);
+      for (uint32_t i = threadIdx.x; i < kSPairs4 * k / 4; i += NT) w4[i] = make_uint4(0, 0, 0, 0);
     }
     __syncthreads();
-    // Per bucket: E = end address of this tile's keys, F = flush bound (last whole sector,
-    // or E at the chunk's end), P = first pending address.  If F > P every old pending key
-    // lies below F and is written now; keys at or above F (all keys when F <= P) wait in
-    // slots relative to max(F, P).  Positions q of the staged tile map to addresses
-    // abase + 8q.
-    for (uint32_t b = threadIdx.x; b < k; b += kSThreads) {
-      const uint64_t cur = abase[b];
-      const uint32_t pl = plen[b];
-      const uint32_t t_off = toff[b], n = toff[b + 1] - t_off;
-      const uint64_t e = cur + 8ull * n;
-      const uint64_t f = last_tile ? e : (e & ~31ull);
-      const uint64_t pb = cur - 8ull * pl;
-      uint64_t s0 = pb;
-      if (f > pb) {
-        for (uint32_t j = 0; j < pl; ++j)
-          __stcs(reinterpret_cast<uint64_t*>(pb) + j, pend[b * kPendSlots + j]);
-        s0 = f;
-      }
-      qlim[b] = (int32_t)t_off + (int32_t)((int64_t)(f - cur) / 8);
-      pbase[b] = (int32_t)t_off + (int32_t)((int64_t)(s0 - cur) / 8);
-      plen[b] = (uint8_t)((e - s0) / 8);
-      abase[b] = cur - 8ull * t_off;
-    }
+    uint32_t bl[kSRounds4];  // bucket | in-warp rank << 16
 #pragma unroll
-    for (int r = 0; r < kSRounds; ++r) {
-      const uint32_t i = wp * (kSRounds * 32) + r * 32 + lane;
+    for (int r = 0; r < kSRounds4; ++r) {
+      const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
+      bl[r] = 0;
       if (i < tl) {
-        const uint32_t pos = toff[bk[r]] + ((wcw[bk[r]] >> wsh) & 0xffffu) + loc[r];
-        stage[pos] = key[r];
-        sbi[pos] = (bk[r] << 16) | i;
+        const uint32_t b = bucket(key[r]);
+        const uint32_t loc = (atomicAdd(&wcw[b], winc) >> wsh) & 0xffffu;
+        bl[r] = b | (loc << 16);
       }
     }
-    {  // prefetch the next tile while this one drains
-      const uint32_t t1 = t0 + kSTile;
+    __syncthreads();
+    // cross-warp exclusive scan per bucket (warp order = key order), then over buckets
+    uint32_t cnt[kCBpt], csum = 0;
 #pragma unroll
-      for (int r = 0; r < kSRounds; ++r) {
-        const uint32_t i = t1 + wp * (kSRounds * 32) + r * 32 + lane;
-        key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
+    for (int q = 0; q < kCBpt; ++q) {
+      const uint32_t b = threadIdx.x * kCBpt + q;
+      uint32_t run = 0;
+      if (b < k) {
+#pragma unroll
+        for (int w2 = 0; w2 < kSPairs4; ++w2) {
+          const uint32_t wv = wc[w2 * k + b];
+          const uint32_t lo = wv & 0xffffu, hi = wv >> 16;
+          wc[w2 * k + b] = run | ((run + lo) << 16);
+          run += lo + hi;
+        }
       }
+      cnt[q] = run;
+      csum += run;
+    }
+    {
+      uint32_t ex = block_exclusive_scan<NT>(csum, s_warp, nullptr);
+#pragma unroll
+      for (int q = 0; q < kCBpt; ++q) {
+        const uint32_t b = threadIdx.x * kCBpt + q;
+        if (b < k) toff[b] = ex;
+        ex += cnt[q];
+      }
+      if (threadIdx.x == NT - 1) toff[k] = ex;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kSRounds4; ++r) {
+      const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
+      if (i < tl) {
+        const uint32_t b = bl[r] & 0xffffu;
+        const uint32_t pos = toff[b] + ((wcw[b] >> wsh) & 0xffffu) + (bl[r] >> 16);
+        stage[pos] = key[r];
+        sbi[pos] = (b << 16) | i;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kSRounds4; ++r) {  // prefetch the next tile while this one drains
+      const uint32_t i = t0 + kSTile4 + wp * (kSRounds4 * 32) + r * 32 + lane;
+      key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
     }
     __syncthreads();
     int bad = 0;
-    for (uint32_t q = threadIdx.x; q < tl; q += kSThreads) {
+    for (uint32_t q = threadIdx.x; q < tl; q += NT) {
       const uint32_t x = sbi[q];
       const uint32_t b = x >> 16;
-      if (q > 0) {
-        const uint32_t y = sbi[q - 1];
-        if ((y >> 16) == b && (y & 0xffffu) > (x & 0xffffu)) bad = 1;
-      }
+      const uint32_t tb = toff[b];
       const uint64_t v = stage[q];
-      if ((int32_t)q < qlim[b]) __stcs(reinterpret_cast<uint64_t*>(abase[b]) + q, v);
-      else pend[b * kPendSlots + (uint32_t)((int32_t)q - pbase[b])] = v;
+      if (q > tb && (sbi[q - 1] & 0xffffu) > (x & 0xffffu)) bad = 1;
+      if (v != stage[tb]) cflag[b] = 2;
+      reinterpret_cast<uint64_t*>(runa[b])[q - tb] = v;
     }
     if (__syncthreads_or(bad)) {
       // Repair (never observed on B200): rewrite every bucket run in tile-index order.
-      for (uint32_t b = threadIdx.x; b < k; b += kSThreads) {
+      for (uint32_t b = threadIdx.x; b < k; b += NT) {
         const uint32_t beg = toff[b], end = toff[b + 1];
         for (uint32_t i = beg + 1; i < end; ++i) {
           const uint32_t xi = sbi[i];
@@ -948,31 +903,54 @@ __device__ void scatter_tiles(const uint64_t* __restrict__ src, uint64_t* __rest
           sbi[j] = xi;
           stage[j] = xv;
         }
-        for (uint32_t q = beg; q < end; ++q) {
-          if ((int32_t)q < qlim[b]) reinterpret_cast<uint64_t*>(abase[b])[q] = stage[q];
-          else pend[b * kPendSlots + (uint32_t)((int32_t)q - pbase[b])] = stage[q];
-        }
+        for (uint32_t q = beg; q < end; ++q) reinterpret_cast<uint64_t*>(runa[b])[q - beg] = stage[q];
       }
       __syncthreads();
     }
-    for (uint32_t b = threadIdx.x; b < k; b += kSThreads) abase[b] += 8ull * toff[b + 1];
+#pragma unroll
+    for (int q = 0; q < kCBpt; ++q) {
+      const uint32_t b = threadIdx.x * kCBpt + q;
+      if (b < k && cnt[q]) {
+        const uint64_t f = stage[toff[b]];
+        const uint8_t cf = cflag[b];
+        if (cf == 0) { ref[b] = f; cflag[b] = 1; }
+        else if (cf == 1 && ref[b] != f) cflag[b] = 2;
+        runa[b] += 8ull * cnt[q];
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < k; b += NT) {
+    const uint8_t cf = cflag[b];
+    a.cflag[(size_t)c * k + b] = cf;
+    if (cf == 1) a.cref[(size_t)c * k + b] = ref[b];
   }
 }
 
 template <bool F64>
-__global__ __launch_bounds__(kSThreads, 2) void k_scatter(
-    const uint64_t* __restrict__ src, uint64_t* __restrict__ dst_user,
-    uint64_t* __restrict__ dst_scr, const ChunkDesc* __restrict__ chunks,
-    const ModelDev* __restrict__ models, uint32_t k, const uint32_t* __restrict__ chunk_pre,
-    const uint64_t* __restrict__ seg_dst, const uint32_t* __restrict__ err) {
-  if (*((volatile const uint32_t*)err) & kErrNan) return;
+__global__ __launch_bounds__(kSThreads4, 2) void k_scatter(LevelArgs a, uint64_t* __restrict__ dst_user,
+                                                           uint64_t* __restrict__ dst_scr) {
+  if (*((volatile const uint32_t*)a.err) & kErrNan) return;
   extern __shared__ __align__(128) unsigned char smraw[];
-  const ChunkDesc ch = chunks[blockIdx.x];
-  const ModelDev md = models[ch.seg];
+  __shared__ OffSmem os;
+  __shared__ uint32_t s_last;
+  const uint32_t c = blockIdx.x;
+  const ChunkDesc ch = a.chunks[c];
+  const ModelDev md = a.models[ch.seg];
   if (md.kind == kModelEq3)
-    scatter_tiles<F64, true>(src, dst_user, dst_scr, ch, md, k, chunk_pre, seg_dst, smraw);
+    scatter_chunk<F64, true>(a, dst_user, dst_scr, c, ch, md, smraw);
   else
-    scatter_tiles<F64, false>(src, dst_user, dst_scr, ch, md, k, chunk_pre, seg_dst, smraw);
+    scatter_chunk<F64, false>(a, dst_user, dst_scr, c, ch, md, smraw);
+  if (a.single_offsets) return;  // ipls_partition_level: no next level
+  const SegDesc sg = a.segs[ch.seg];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(&a.seg_done[ch.seg], 1u) == sg.nchunks - 1) ? 1u : 0u;
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    segment_emit(a, ch.seg, sg, md, os, reinterpret_cast<uint32_t*>(smraw));
+  }
 }
 
 // ------------------------------------------------------------------------------------
