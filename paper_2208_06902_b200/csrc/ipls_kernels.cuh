@@ -23,10 +23,10 @@ constexpr int kFitMaxS = 8192;
 constexpr int kBaseMax = 8192;                 // keys per base-case window (W + B)
 constexpr uint32_t kMaxK = 1024;
 // small-window base case (k_base_warp)
-constexpr int kWBCap = 512;                      // keys per warp window
+constexpr int kWBCap = 256;                      // keys per warp window
 constexpr int kWBBinsPerKey = 2;
 constexpr int kWBBins = kWBBinsPerKey * kWBCap;  // fine bins per warp
-constexpr int kWBWarps = 12;                     // warps per CTA, one CTA per SM
+constexpr int kWBWarps = 24;                     // warps per CTA, one CTA per SM
 constexpr int kWBStride = kWBCap + 4;            // keys per prefetch buffer (+ alignment slack)
 constexpr size_t kWBSmemPerWarp =
     (size_t)2 * kWBStride * 8 + kWBCap * 8 + kWBCap * 4 + (kWBBins + 32) * 4;
@@ -366,11 +366,13 @@ __host__ __device__ constexpr size_t win_scratch_bytes(uint32_t k) {
 // within cap keys (binary search); J(c) = first selected child after jump(c); the window
 // starts are the orbit of the first selected child under J, marked by pointer doubling
 // (log2 k rounds).  Appends the windows to `out` (global counter `cnt`, keys to `keys`).
+template <int NT>
 __device__ void pack_windows(const LevelArgs& a, const SegDesc& sg, uint32_t k,
-                             const uint32_t (&bb)[kCBpt], const uint32_t (&base)[kCBpt],
-                             const uint32_t (&tot)[kCBpt], const bool (&sel)[kCBpt], uint32_t cap,
+                             const uint32_t (&bb)[kMaxK / NT], const uint32_t (&base)[kMaxK / NT],
+                             const uint32_t (&tot)[kMaxK / NT], const bool (&sel)[kMaxK / NT], uint32_t cap,
                              uint32_t dstbuf, OffSmem& os, uint32_t* wsm, Window* out,
                              uint32_t out_cap, uint32_t* cnt, uint64_t* keys) {
+  constexpr int BPT = kMaxK / NT;
   const uint32_t K1 = k + 1;
   uint32_t* w_start = wsm;
   uint32_t* w_end = wsm + K1;
@@ -382,16 +384,16 @@ __device__ void pack_windows(const LevelArgs& a, const SegDesc& sg, uint32_t k,
   uint32_t* w_mark = wsm + 7 * K1;
   uint32_t nbrk = 0, nsel = 0;
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
+  for (int q = 0; q < BPT; ++q) {
     nbrk += (bb[q] < k && tot[q] && !sel[q]) ? 1u : 0u;
     nsel += sel[q] ? 1u : 0u;
   }
   uint32_t t_sel;
-  uint32_t brk_run = block_exclusive_scan<kCThreads>(nbrk, os.warp, nullptr);
-  uint32_t sel_run = block_exclusive_scan<kCThreads>(nsel, os.warp, &t_sel);
+  uint32_t brk_run = block_exclusive_scan<NT>(nbrk, os.warp, nullptr);
+  uint32_t sel_run = block_exclusive_scan<NT>(nsel, os.warp, &t_sel);
   if (t_sel == 0) return;  // block-uniform
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
+  for (int q = 0; q < BPT; ++q) {
     if (bb[q] < k) {
       brk_run += (tot[q] && !sel[q]) ? 1u : 0u;
       if (sel[q]) w_idx[sel_run] = bb[q];
@@ -406,7 +408,7 @@ __device__ void pack_windows(const LevelArgs& a, const SegDesc& sg, uint32_t k,
   if (threadIdx.x == 0) { w_J[k] = k; w_mark[k] = 0u; }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
+  for (int q = 0; q < BPT; ++q) {
     if (sel[q]) {
       const uint32_t c = bb[q], st0 = base[q], bk0 = w_brk[c];
       uint32_t lo = c, hi = k;
@@ -424,9 +426,9 @@ __device__ void pack_windows(const LevelArgs& a, const SegDesc& sg, uint32_t k,
   if (threadIdx.x == 0) w_mark[w_idx[0]] = 1u;
   __syncthreads();
   for (uint32_t span = 1; span < t_sel; span <<= 1) {
-    uint32_t mk[kCBpt], jj[kCBpt], j2[kCBpt];
+    uint32_t mk[BPT], jj[BPT], j2[BPT];
 #pragma unroll
-    for (int q = 0; q < kCBpt; ++q) {
+    for (int q = 0; q < BPT; ++q) {
       mk[q] = 0; jj[q] = k; j2[q] = k;
       if (bb[q] < k) {
         mk[q] = w_mark[bb[q]];
@@ -436,7 +438,7 @@ __device__ void pack_windows(const LevelArgs& a, const SegDesc& sg, uint32_t k,
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < kCBpt; ++q) {
+    for (int q = 0; q < BPT; ++q) {
       if (mk[q] && jj[q] < k) w_mark[jj[q]] = 1u;
       if (bb[q] < k) w_J[bb[q]] = j2[q];
     }
@@ -444,13 +446,13 @@ __device__ void pack_windows(const LevelArgs& a, const SegDesc& sg, uint32_t k,
   }
   uint32_t nw = 0;
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) nw += (sel[q] && w_mark[bb[q]]) ? 1u : 0u;
+  for (int q = 0; q < BPT; ++q) nw += (sel[q] && w_mark[bb[q]]) ? 1u : 0u;
   uint32_t t_w;
-  uint32_t w_off = block_exclusive_scan<kCThreads>(nw, os.warp, &t_w);
+  uint32_t w_off = block_exclusive_scan<NT>(nw, os.warp, &t_w);
   if (threadIdx.x == 0) os.res[4] = atomicAdd(cnt, t_w);
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
+  for (int q = 0; q < BPT; ++q) {
     if (sel[q] && w_mark[bb[q]]) {
       const uint32_t gi = os.res[4] + w_off++;
       if (gi < out_cap) {
@@ -501,15 +503,17 @@ __device__ void segment_bases(const LevelArgs& a, uint32_t s, const SegDesc& sg,
 // the per-(chunk, bucket) flags the scatter recorded: a child is homogeneous iff every chunk
 // that holds keys of it saw one value and all those values agree.  Only children above the
 // base case can be classed homogeneous-final, so only they are merged.
+template <int NT>
 __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, const ModelDev& md,
                              OffSmem& os, uint32_t* wsm) {
+  constexpr int BPT = kMaxK / NT;
   const uint32_t k = a.k;
-  uint32_t bb[kCBpt], base[kCBpt], tot[kCBpt], inh[kCBpt];
-  uint64_t rep[kCBpt];
+  uint32_t bb[BPT], base[BPT], tot[BPT], inh[BPT];
+  uint64_t rep[BPT];
   uint32_t x = 0;
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
-    bb[q] = threadIdx.x * kCBpt + q;
+  for (int q = 0; q < BPT; ++q) {
+    bb[q] = threadIdx.x * BPT + q;
     tot[q] = (bb[q] < k) ? a.seg_tot[(size_t)s * k + bb[q]] : 0u;
     x += tot[q];
     inh[q] = 1;
@@ -531,18 +535,18 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
       rep[q] = ref;
     }
   }
-  uint32_t ex = block_exclusive_scan<kCThreads>(x, os.warp, nullptr);
+  uint32_t ex = block_exclusive_scan<NT>(x, os.warp, nullptr);
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) { base[q] = ex; ex += tot[q]; }
+  for (int q = 0; q < BPT; ++q) { base[q] = ex; ex += tot[q]; }
   int st = 0;
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q)
+  for (int q = 0; q < BPT; ++q)
     if (md.kind == kModelLinear && bb[q] < k && tot[q] == sg.m) st = 1;
   const bool stuck = __syncthreads_or(st) != 0;
   const uint32_t dstbuf = (a.level + 1) & 1;  // 1 = scratch, 0 = user array
-  uint32_t cls[kCBpt];
+  uint32_t cls[BPT];
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
+  for (int q = 0; q < BPT; ++q) {
     cls[q] = 0;  // 0 empty, 1 base (or small homogeneous), 2 partition, 3 big homogeneous
     if (!stuck && bb[q] < k && tot[q] > 0) {
       const bool homog = (md.kind == kModelEq3 && bb[q] == 1) || !inh[q];
@@ -553,9 +557,9 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
   }
   // ---- next-level segments ----
   uint32_t w_seg = 0, w_samp = 0, w_ch = 0;
-  uint32_t cm[kCBpt];
+  uint32_t cm[BPT];
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
+  for (int q = 0; q < BPT; ++q) {
     cm[q] = 0;
     if (stuck) { if (threadIdx.x == 0 && q == 0) cm[q] = sg.m; }
     else if (cls[q] == 2) cm[q] = tot[q];
@@ -566,9 +570,9 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
     }
   }
   uint32_t t_seg, t_samp, t_ch;
-  uint32_t o_seg = block_exclusive_scan<kCThreads>(w_seg, os.warp, &t_seg);
-  uint32_t o_samp = block_exclusive_scan<kCThreads>(w_samp, os.warp, &t_samp);
-  uint32_t o_ch = block_exclusive_scan<kCThreads>(w_ch, os.warp, &t_ch);
+  uint32_t o_seg = block_exclusive_scan<NT>(w_seg, os.warp, &t_seg);
+  uint32_t o_samp = block_exclusive_scan<NT>(w_samp, os.warp, &t_samp);
+  uint32_t o_ch = block_exclusive_scan<NT>(w_ch, os.warp, &t_ch);
   if (threadIdx.x == 0 && t_seg) {
     os.res[0] = atomicAdd(&a.nctr->n_segs, t_seg);
     os.res[1] = atomicAdd(&a.nctr->n_samples, t_samp);
@@ -583,7 +587,7 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
     } else {
       uint32_t i_seg = os.res[0] + o_seg, i_samp = os.res[1] + o_samp, i_ch = os.res[2] + o_ch;
 #pragma unroll
-      for (int q = 0; q < kCBpt; ++q) {
+      for (int q = 0; q < BPT; ++q) {
         if (cm[q]) {
           uint64_t cb = stuck ? sg.begin : sg.begin + base[q];
           emit_segment(a, cb, cm[q], stuck ? kSegForceEq3 : 0u, i_seg, i_samp, i_ch);
@@ -601,27 +605,27 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
   // (sorted by k_base_warp); base children above kWBCap ("big") into windows of <= kBaseMax
   // keys (k_base_sort).  Every other child breaks a window.
   {
-    bool small[kCBpt], bigb[kCBpt];
+    bool small[BPT], bigb[BPT];
 #pragma unroll
-    for (int q = 0; q < kCBpt; ++q) {
+    for (int q = 0; q < BPT; ++q) {
       small[q] = bb[q] < k && cls[q] == 1 && tot[q] <= (uint32_t)kWBCap;
       bigb[q] = bb[q] < k && cls[q] == 1 && tot[q] > (uint32_t)kWBCap;
     }
-    pack_windows(a, sg, k, bb, base, tot, small, (uint32_t)kWBCap, dstbuf, os, wsm, a.wins,
+    pack_windows<NT>(a, sg, k, bb, base, tot, small, (uint32_t)kWBCap, dstbuf, os, wsm, a.wins,
                  a.cap_wins, &a.nctr->n_windows, &a.nctr->win_keys);
-    pack_windows(a, sg, k, bb, base, tot, bigb, (uint32_t)kBaseMax, dstbuf, os, wsm, a.wins_big,
+    pack_windows<NT>(a, sg, k, bb, base, tot, bigb, (uint32_t)kBaseMax, dstbuf, os, wsm, a.wins_big,
                  a.cap_wbig, &a.nctr->n_wbig, &a.nctr->wbig_keys);
   }
   // ---- homogeneous children that land in scratch must be filled into the user array ----
   uint32_t nf = 0;
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) nf += (cls[q] == 3 && dstbuf == 1) ? 1u : 0u;
+  for (int q = 0; q < BPT; ++q) nf += (cls[q] == 3 && dstbuf == 1) ? 1u : 0u;
   uint32_t t_fill;
-  uint32_t o_fill = block_exclusive_scan<kCThreads>(nf, os.warp, &t_fill);
+  uint32_t o_fill = block_exclusive_scan<NT>(nf, os.warp, &t_fill);
   if (threadIdx.x == 0 && t_fill) os.res[5] = atomicAdd(&a.nctr->n_fills, t_fill);
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < kCBpt; ++q) {
+  for (int q = 0; q < BPT; ++q) {
     if (cls[q] == 3 && dstbuf == 1) {
       uint32_t gi = os.res[5] + o_fill++;
       if (gi < a.cap_fills) {
@@ -752,9 +756,9 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
 }
 
 // ------------------------------------------------------------------------------------
-// Phase 4b: stable scatter of one chunk (R11), 512 threads, 2 CTAs per SM.
+// Phase 4b: stable scatter of one chunk (R11), 1024 threads, 1 CTA per SM.
 //
-// Tile = 4096 keys; warp w owns keys [256w, 256w+256) in 8 rounds of 32.
+// Tile = 8192 keys; warp w owns keys [256w, 256w+256) in 8 rounds of 32.
 // Rank: every key does one smem atomicAdd on its warp's counter for its bucket (u16 halves
 // of packed u32 words, two warps per word).  Same-address lanes of one atomic instruction
 // are served in lane order on B200 (tools/micro/atom_order.cu: 0 violations in 2.2e9 lane
@@ -770,9 +774,10 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
 // per-bucket pass after the write-out compares that key with the chunk's first key of the
 // bucket.  The chunk's flags (0 empty, 1 one value, 2 several) and values go to global memory
 // for segment_emit.
-constexpr int kSThreads4 = 512;
-constexpr int kSWarps4 = kSThreads4 / 32;          // 16
+constexpr int kSThreads4 = 1024;
+constexpr int kSWarps4 = kSThreads4 / 32;          // 32
 constexpr int kSRounds4 = 8;                       // keys per thread per tile
+constexpr int kSBpt = kMaxK / kSThreads4;          // buckets per thread in the scans
 constexpr int kSTile4 = kSThreads4 * kSRounds4;    // 4096
 constexpr int kSPairs4 = kSWarps4 / 2;             // warp pairs sharing a counter word
 
@@ -833,10 +838,10 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
     }
     __syncthreads();
     // cross-warp exclusive scan per bucket (warp order = key order), then over buckets
-    uint32_t cnt[kCBpt], csum = 0;
+    uint32_t cnt[kSBpt], csum = 0;
 #pragma unroll
-    for (int q = 0; q < kCBpt; ++q) {
-      const uint32_t b = threadIdx.x * kCBpt + q;
+    for (int q = 0; q < kSBpt; ++q) {
+      const uint32_t b = threadIdx.x * kSBpt + q;
       uint32_t run = 0;
       if (b < k) {
 #pragma unroll
@@ -853,8 +858,8 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
     {
       uint32_t ex = block_exclusive_scan<NT>(csum, s_warp, nullptr);
 #pragma unroll
-      for (int q = 0; q < kCBpt; ++q) {
-        const uint32_t b = threadIdx.x * kCBpt + q;
+      for (int q = 0; q < kSBpt; ++q) {
+        const uint32_t b = threadIdx.x * kSBpt + q;
         if (b < k) toff[b] = ex;
         ex += cnt[q];
       }
@@ -908,8 +913,8 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
       __syncthreads();
     }
 #pragma unroll
-    for (int q = 0; q < kCBpt; ++q) {
-      const uint32_t b = threadIdx.x * kCBpt + q;
+    for (int q = 0; q < kSBpt; ++q) {
+      const uint32_t b = threadIdx.x * kSBpt + q;
       if (b < k && cnt[q]) {
         const uint64_t f = stage[toff[b]];
         const uint8_t cf = cflag[b];
@@ -928,7 +933,7 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
 }
 
 template <bool F64>
-__global__ __launch_bounds__(kSThreads4, 2) void k_scatter(LevelArgs a, uint64_t* __restrict__ dst_user,
+__global__ __launch_bounds__(kSThreads4, 1) void k_scatter(LevelArgs a, uint64_t* __restrict__ dst_user,
                                                            uint64_t* __restrict__ dst_scr) {
   if (*((volatile const uint32_t*)a.err) & kErrNan) return;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -949,7 +954,7 @@ __global__ __launch_bounds__(kSThreads4, 2) void k_scatter(LevelArgs a, uint64_t
   __syncthreads();
   if (s_last) {
     __threadfence();
-    segment_emit(a, ch.seg, sg, md, os, reinterpret_cast<uint32_t*>(smraw));
+    segment_emit<kSThreads4>(a, ch.seg, sg, md, os, reinterpret_cast<uint32_t*>(smraw));
   }
 }
 
@@ -1442,34 +1447,45 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
         warp_bitonic_ok<F64>(B, len, lane);
         OUT = B;
       } else {
-        // bins hold bin ends now; every key ranks itself among its bin and lands in INb
-        // (the input copy is dead: keys are read back from B).
+        // bins hold bin ends now.  Keys alone in their bin are already in place in B.  Keys
+        // of multi-key bins (a minority) are compacted into a worklist (in place over FS);
+        // each ranks itself among its bin (smaller, or equal at a smaller slot) and is
+        // written to INb (dead input copy) at bin start + rank, then copied back to B.
+        uint32_t nwork = 0;
         for (uint32_t base = 0; base < len; base += 32) {
           const uint32_t i = base + lane;
-          const bool valid = i < len;
-          uint32_t fb = 0, slot = 0, beg = 0, end = 0;
-          uint64_t x = 0;
-          if (valid) {
+          uint32_t item = 0;
+          bool multi = false;
+          if (i < len) {
             const uint32_t w = FS[i];
-            fb = w & 0xffffu;
-            slot = w >> 16;
-            beg = (fb % (BPL + 1)) ? bins[fb - 1] : (fb ? bins[fb - 2] : 0u);
-            end = bins[fb];
-            x = B[slot];
+            const uint32_t fb = w & 0xffffu, slot = w >> 16;
+            const uint32_t beg = (fb % (BPL + 1)) ? bins[fb - 1] : (fb ? bins[fb - 2] : 0u);
+            const uint32_t end = bins[fb];
+            multi = end - beg > 1;
+            item = slot | (beg << 10) | ((end - beg) << 20);
           }
-          const uint32_t n = __reduce_max_sync(0xffffffffu, end - beg);
-          uint32_t r = beg;
-          for (uint32_t q = 1; q < n; ++q) {  // n == 1: every key is alone in its bin
-            const uint32_t p0 = beg + q - 1;
-            const uint32_t p = p0 < slot ? p0 : p0 + 1;  // skip the key's own slot
-            if (p < end) {
-              const uint64_t y = B[p];
-              r += (key_before<F64>(y, x) || (y == x && p < slot)) ? 1u : 0u;
-            }
-          }
-          if (valid) INb[r] = x;
+          const uint32_t mask = __ballot_sync(0xffffffffu, multi);
+          if (multi) FS[nwork + __popc(mask & ((1u << lane) - 1u))] = item;
+          nwork += __popc(mask);
         }
-        OUT = INb;
+        __syncwarp();
+        for (uint32_t j = lane; j < nwork; j += 32) {
+          const uint32_t item = FS[j];
+          const uint32_t slot = item & 1023u, beg = (item >> 10) & 1023u, n = item >> 20;
+          const uint64_t x = B[slot];
+          uint32_t r = beg;
+          for (uint32_t p = beg; p < beg + n; ++p) {
+            const uint64_t y = B[p];
+            r += (p != slot && (key_before<F64>(y, x) || (y == x && p < slot))) ? 1u : 0u;
+          }
+          INb[r] = x;
+        }
+        __syncwarp();
+        for (uint32_t j = lane; j < nwork; j += 32) {
+          const uint32_t slot = FS[j] & 1023u;
+          B[slot] = INb[slot];
+        }
+        OUT = B;
       }
     }
     __syncwarp();
