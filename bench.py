@@ -220,7 +220,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--traffic", type=float, default=None,
-                    help="ncu dram bytes per launch of the dominant kernel (from profiles/)")
+                    help="ncu dram bytes per launch of the dominant kernel (default: the "
+                         "committed profiles/r01_traffic.json capture)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -289,6 +290,13 @@ def main():
     dom = max((k_ for k_ in prof if prof[k_][2] > 0), key=lambda k_: prof[k_][1])
     d_launch, d_ms, d_bytes = prof[dom]
     achieved = d_bytes / (d_ms / 1e3) / 1e9
+    traffic = args.traffic
+    if traffic is None:
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+                traffic = json.load(f)["kernels"][dom]["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
     shares = {k_: round(v[1] / tot_prof_ms, 4) for k_, v in sorted(prof.items())}
     per_kernel = {k_: {"launches": v[0], "ms_per_step": round(v[1] / args.steps, 4),
                        "alg_GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1) if v[2] > 0 else None}
@@ -345,7 +353,8 @@ def main():
             },
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": args.traffic},
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "alg_bytes_per_launch": d_bytes / max(d_launch, 1)},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n},
