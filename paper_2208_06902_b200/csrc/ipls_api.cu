@@ -781,6 +781,17 @@ const char* ipls_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
 
 uint64_t ipls_kernel_launch_count(void) { return g_launches.load(); }
 
+#ifdef IPLS_SCATTER_TIMING
+// dev builds only (tools/phase_scatter.py): per-phase cycle sums of thread 0 of every CTA
+void ipls_debug_scatter_phases(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_sc_phase, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_sc_phase, z, sizeof(z));
+  }
+}
+#endif
+
 void ipls_profile_enable(int on) { g_prof_on.store(on ? 1 : 0); }
 
 void ipls_profile_reset(void) {

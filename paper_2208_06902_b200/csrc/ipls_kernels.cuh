@@ -774,6 +774,9 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
 // per-bucket pass after the write-out compares that key with the chunk's first key of the
 // bucket.  The chunk's flags (0 empty, 1 one value, 2 several) and values go to global memory
 // for segment_emit.
+#ifdef IPLS_SCATTER_TIMING
+__device__ unsigned long long g_sc_phase[16];
+#endif
 constexpr int kSThreads4 = 1024;
 constexpr int kSWarps4 = kSThreads4 / 32;          // 32
 constexpr int kSRounds4 = 8;                       // keys per thread per tile
@@ -782,7 +785,7 @@ constexpr int kSTile4 = kSThreads4 * kSRounds4;    // 4096
 constexpr int kSPairs4 = kSWarps4 / 2;             // warp pairs sharing a counter word
 
 __host__ __device__ constexpr size_t scatter_smem_bytes(uint32_t k) {
-  return (size_t)kSTile4 * 8 + (size_t)k * 8 + (size_t)k * 8 + (size_t)kSTile4 * 4 +
+  return (size_t)kSTile4 * 8 + (size_t)k * 8 * 3 + (size_t)kSTile4 * 4 +
          (size_t)kSPairs4 * k * 4 + (size_t)(k + 1) * 4 + (size_t)k + 16;
 }
 
@@ -793,11 +796,12 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
   constexpr int NT = kSThreads4;
   const uint32_t k = a.k;
   uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);         // kSTile4
-  uint64_t* runa = stage + kSTile4;                              // k: byte address of next write
+  uint32_t* wc = reinterpret_cast<uint32_t*>(stage + kSTile4);   // kSPairs4 * k (16-B multiple)
+  uint64_t* runa = reinterpret_cast<uint64_t*>(wc + kSPairs4 * k);  // k: byte address of next write
   uint64_t* ref = runa + k;                                      // k: chunk's first key
-  uint32_t* sbi = reinterpret_cast<uint32_t*>(ref + k);          // kSTile4: bucket << 16 | index
-  uint32_t* wc = sbi + kSTile4;                                  // kSPairs4 * k
-  uint32_t* toff = wc + kSPairs4 * k;                            // k + 1
+  uint64_t* adj = ref + k;                                       // k: runa - 8 * tile offset
+  uint32_t* sbi = reinterpret_cast<uint32_t*>(adj + k);          // kSTile4: bucket << 16 | index
+  uint32_t* toff = sbi + kSTile4;                                // k + 1
   uint8_t* cflag = reinterpret_cast<uint8_t*>(toff + k + 1);     // k
   __shared__ uint32_t s_warp[40];
   const Bucketer<F64, EQ3> bucket(md, k);
@@ -818,6 +822,12 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
     const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
     key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
   }
+#ifdef IPLS_SCATTER_TIMING
+  long long t_prev_ = clock64();
+#define SC_TICK(N) do { if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_sc_phase[N], (unsigned long long)(t_ - t_prev_)); t_prev_ = t_; } } while (0)
+#else
+#define SC_TICK(N)
+#endif
   for (uint32_t t0 = 0; t0 < ch.len; t0 += kSTile4) {
     const uint32_t tl = min((uint32_t)kSTile4, ch.len - t0);
     {
@@ -825,6 +835,7 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
       for (uint32_t i = threadIdx.x; i < kSPairs4 * k / 4; i += NT) w4[i] = make_uint4(0, 0, 0, 0);
     }
     __syncthreads();
+    SC_TICK(0);
     uint32_t bl[kSRounds4];  // bucket | in-warp rank << 16
 #pragma unroll
     for (int r = 0; r < kSRounds4; ++r) {
@@ -837,7 +848,10 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
       }
     }
     __syncthreads();
-    // cross-warp exclusive scan per bucket (warp order = key order), then over buckets
+    SC_TICK(1);
+    // Per bucket: tile count (sum over the warps), scan over buckets, then every warp's word
+    // becomes the absolute staged position of its first key of the bucket (tile offset +
+    // exclusive prefix over the earlier warps: warp order = key order).
     uint32_t cnt[kSBpt], csum = 0;
 #pragma unroll
     for (int q = 0; q < kSBpt; ++q) {
@@ -847,9 +861,7 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
 #pragma unroll
         for (int w2 = 0; w2 < kSPairs4; ++w2) {
           const uint32_t wv = wc[w2 * k + b];
-          const uint32_t lo = wv & 0xffffu, hi = wv >> 16;
-          wc[w2 * k + b] = run | ((run + lo) << 16);
-          run += lo + hi;
+          run += (wv & 0xffffu) + (wv >> 16);
         }
       }
       cnt[q] = run;
@@ -860,18 +872,30 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
 #pragma unroll
       for (int q = 0; q < kSBpt; ++q) {
         const uint32_t b = threadIdx.x * kSBpt + q;
-        if (b < k) toff[b] = ex;
+        if (b < k) {
+          toff[b] = ex;
+          adj[b] = runa[b] - 8ull * ex;
+          uint32_t run = ex;
+#pragma unroll
+          for (int w2 = 0; w2 < kSPairs4; ++w2) {
+            const uint32_t wv = wc[w2 * k + b];
+            const uint32_t lo = wv & 0xffffu, hi = wv >> 16;
+            wc[w2 * k + b] = run | ((run + lo) << 16);
+            run += lo + hi;
+          }
+        }
         ex += cnt[q];
       }
       if (threadIdx.x == NT - 1) toff[k] = ex;
     }
     __syncthreads();
+    SC_TICK(2);
 #pragma unroll
     for (int r = 0; r < kSRounds4; ++r) {
       const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
       if (i < tl) {
         const uint32_t b = bl[r] & 0xffffu;
-        const uint32_t pos = toff[b] + ((wcw[b] >> wsh) & 0xffffu) + (bl[r] >> 16);
+        const uint32_t pos = ((wcw[b] >> wsh) & 0xffffu) + (bl[r] >> 16);
         stage[pos] = key[r];
         sbi[pos] = (b << 16) | i;
       }
@@ -882,16 +906,25 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
       key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
     }
     __syncthreads();
+    SC_TICK(3);
+    // Write-out: staged key q goes to adj[bucket] + 8 q.  Its staged predecessor decides the
+    // stability check (same bucket => increasing tile index) and the in-tile homogeneity check
+    // (same bucket => same value); both are sequential smem reads.
     int bad = 0;
     for (uint32_t q = threadIdx.x; q < tl; q += NT) {
       const uint32_t x = sbi[q];
       const uint32_t b = x >> 16;
-      const uint32_t tb = toff[b];
       const uint64_t v = stage[q];
-      if (q > tb && (sbi[q - 1] & 0xffffu) > (x & 0xffffu)) bad = 1;
-      if (v != stage[tb]) cflag[b] = 2;
-      reinterpret_cast<uint64_t*>(runa[b])[q - tb] = v;
+      if (q > 0) {
+        const uint32_t y = sbi[q - 1];
+        if ((y >> 16) == b) {
+          if ((y & 0xffffu) > (x & 0xffffu)) bad = 1;
+          if (stage[q - 1] != v) cflag[b] = 2;
+        }
+      }
+      reinterpret_cast<uint64_t*>(adj[b])[q] = v;
     }
+    SC_TICK(4);
     if (__syncthreads_or(bad)) {
       // Repair (never observed on B200): rewrite every bucket run in tile-index order.
       for (uint32_t b = threadIdx.x; b < k; b += NT) {
@@ -912,6 +945,7 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
       }
       __syncthreads();
     }
+    SC_TICK(5);
 #pragma unroll
     for (int q = 0; q < kSBpt; ++q) {
       const uint32_t b = threadIdx.x * kSBpt + q;
@@ -923,6 +957,7 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
         runa[b] += 8ull * cnt[q];
       }
     }
+    SC_TICK(6);
   }
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < k; b += NT) {
