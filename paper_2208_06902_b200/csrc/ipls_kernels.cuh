@@ -1351,17 +1351,16 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
   uint32_t* bins = FS + kWBCap;                                              // kWBBins + 32
   uint64_t* mbar = s_mbar[wp];
   const uint32_t gw = blockIdx.x * kWBWarps + wp, gstride = gridDim.x * kWBWarps;
-  auto fetch = [&](uint32_t w, int b, Window& wv) {  // lane 0: bulk copy of window w -> IN[b]
-    if (lane == 0 && w < nwin) {
-      wv = wins[w];
-      const uint64_t* g = (wv.buf ? scr : user) + wv.begin;
-      const WinGeom gm = win_geom(g, wv.len);
-      if (gm.body) {
-        mbar_arrive_tx(&mbar[b], gm.body * 8u);
-        bulk_g2s(IN + (size_t)b * kWBStride + 2, g + gm.head, gm.body * 8u, &mbar[b]);
-      } else {
-        mbar_arrive(&mbar[b]);
-      }
+  // lane 0: start the bulk copy of the window described by wv into IN[b].  Descriptors are
+  // loaded two windows ahead so that their global latency is off the critical path.
+  auto issue = [&](const Window& wv, int b) {
+    const uint64_t* g = (wv.buf ? scr : user) + wv.begin;
+    const WinGeom gm = win_geom(g, wv.len);
+    if (gm.body) {
+      mbar_arrive_tx(&mbar[b], gm.body * 8u);
+      bulk_g2s(IN + (size_t)b * kWBStride + 2, g + gm.head, gm.body * 8u, &mbar[b]);
+    } else {
+      mbar_arrive(&mbar[b]);
     }
   };
   if (lane == 0) {
@@ -1370,15 +1369,30 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  Window nwv{};
-  fetch(gw, 0, nwv);
+#ifdef IPLS_BASE_TIMING
+  long long t_prev_ = clock64();
+  unsigned long long acc_[10] = {0};
+#define WB_TICK(N) do { const long long t_ = clock64(); acc_[N] += (unsigned long long)(t_ - t_prev_); t_prev_ = t_; } while (0)
+#else
+#define WB_TICK(N)
+#endif
+  Window d_cur{}, d_nxt{};  // lane 0: descriptors of windows cur and cur+1 (in flight)
+  if (lane == 0) {
+    if (gw < nwin) { d_cur = wins[gw]; issue(d_cur, 0); }
+    if (gw + gstride < nwin) d_nxt = wins[gw + gstride];
+  }
   for (uint32_t it = 0, cur = gw; cur < nwin; ++it, cur += gstride) {
     const int b = it & 1;
     Window wv;
-    wv.begin = __shfl_sync(0xffffffffu, nwv.begin, 0);
-    wv.len = __shfl_sync(0xffffffffu, nwv.len, 0);
-    wv.buf = __shfl_sync(0xffffffffu, nwv.buf, 0);
-    fetch(cur + gstride, b ^ 1, nwv);
+    wv.begin = __shfl_sync(0xffffffffu, d_cur.begin, 0);
+    wv.len = __shfl_sync(0xffffffffu, d_cur.len, 0);
+    wv.buf = __shfl_sync(0xffffffffu, d_cur.buf, 0);
+    if (lane == 0) {
+      d_cur = d_nxt;  // loaded one window ago
+      if (cur + gstride < nwin) issue(d_cur, b ^ 1);
+      if (cur + 2 * gstride < nwin) d_nxt = wins[cur + 2 * gstride];  // consumed next window
+    }
+    WB_TICK(0);
     const uint32_t len = wv.len;
     const uint64_t* src = (wv.buf ? scr : user) + wv.begin;
     uint64_t* dst = user + wv.begin;
@@ -1389,6 +1403,7 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     if (lane == 1 && gm.tail) K[len - 1] = __ldcs(src + len - 1);
     mbar_wait(&mbar[b], (it >> 1) & 1);
     __syncwarp();
+    WB_TICK(1);
     // ---- bounds ----
     double mn = 0.0, range;
     uint64_t umn = ~0ull, umx = 0ull;
@@ -1420,6 +1435,7 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       range = (double)(umx - umn);
     }
     const uint64_t* OUT = K;  // constant (u64) windows are already sorted
+    WB_TICK(2);
     if (!F64 && umn == umx) {
       // nothing to sort
     } else if (!(range > 0.0) || !(range < 1.79e308)) {  // +-0 mixes, infinities, overflow
@@ -1430,7 +1446,7 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     } else {
       const uint32_t nb = kWBBinsPerKey * len;
       const double scale = (double)nb / range;
-      // Bin f lives at bins[f + f / BPL] (one pad word per lane-owned group) so that the
+      // Bin f lives at bins[f + f / 32] (one pad word per 32 bins) so that the
       // lane-contiguous scan walk is conflict-free.
       for (uint32_t q = lane; q < (uint32_t)(kWBBins + 32); q += 32) bins[q] = 0u;
       __syncwarp();
@@ -1440,14 +1456,14 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
         if constexpr (F64) y = __longlong_as_double((long long)x) - mn;
         else y = (double)(x - umn);
         uint32_t fb = min(__double2uint_rz(y * scale), nb - 1);
-        fb += fb / BPL;
-        FS[i] = fb;
-        atomicAdd(&bins[fb], 1u);
+        FS[i] = fb;  // unpadded bin
+        atomicAdd(&bins[fb + (fb >> 5)], 1u);
       }
       __syncwarp();
+    WB_TICK(3);
       uint32_t mxc = 0;
       {
-        uint32_t* bl0 = bins + lane * (BPL + 1);
+        uint32_t* bl0 = bins + lane * BPL + ((lane * BPL) >> 5);
         uint32_t sum = 0;
 #pragma unroll 8
         for (int q = 0; q < BPL; ++q) {
@@ -1471,13 +1487,15 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       }
       const bool overflow = __any_sync(0xffffffffu, mxc > kFineOverflow);
       __syncwarp();
+    WB_TICK(4);
       for (uint32_t i = lane; i < len; i += 32) {
         const uint32_t fb = FS[i];
-        const uint32_t slot = atomicAdd(&bins[fb], 1u);
+        const uint32_t slot = atomicAdd(&bins[fb + (fb >> 5)], 1u);
         B[slot] = K[i];
         FS[i] = fb | (slot << 16);
       }
       __syncwarp();
+    WB_TICK(5);
       if (overflow) {
         warp_bitonic_ok<F64>(B, len, lane);
         OUT = B;
@@ -1494,8 +1512,8 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
           if (i < len) {
             const uint32_t w = FS[i];
             const uint32_t fb = w & 0xffffu, slot = w >> 16;
-            const uint32_t beg = (fb % (BPL + 1)) ? bins[fb - 1] : (fb ? bins[fb - 2] : 0u);
-            const uint32_t end = bins[fb];
+            const uint32_t beg = fb ? bins[(fb - 1) + ((fb - 1) >> 5)] : 0u;
+            const uint32_t end = bins[fb + (fb >> 5)];
             multi = end - beg > 1;
             item = slot | (beg << 10) | ((end - beg) << 20);
           }
@@ -1504,6 +1522,7 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
           nwork += __popc(mask);
         }
         __syncwarp();
+    WB_TICK(6);
         for (uint32_t j = lane; j < nwork; j += 32) {
           const uint32_t item = FS[j];
           const uint32_t slot = item & 1023u, beg = (item >> 10) & 1023u, n = item >> 20;
@@ -1516,6 +1535,7 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
           INb[r] = x;
         }
         __syncwarp();
+    WB_TICK(7);
         for (uint32_t j = lane; j < nwork; j += 32) {
           const uint32_t slot = FS[j] & 1023u;
           B[slot] = INb[slot];
@@ -1525,9 +1545,14 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     }
     __syncwarp();
     for (uint32_t i = lane; i < len; i += 32) __stcs(dst + i, OUT[i]);
+    WB_TICK(8);
     fence_proxy_async_smem();  // generic accesses to IN[b] before the bulk copy that reuses it
     __syncwarp();
   }
+#ifdef IPLS_BASE_TIMING
+  if (lane == 0)
+    for (int q = 0; q < 10; ++q) atomicAdd(&g_base_phase[q], acc_[q]);
+#endif
 }
 
 __global__ void k_fill(const Fill* __restrict__ fills, uint64_t* __restrict__ user) {

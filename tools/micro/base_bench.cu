@@ -25,7 +25,7 @@ __global__ void chk(const double* a, uint64_t n, uint32_t* bad) {
 
 int main(int argc, char** argv) {
   const uint64_t n = 100000000ull;
-  for (uint32_t W : {256u, 450u, 512u, 2048u, 4096u, 8192u}) {
+  for (uint32_t W : {200u, 256u, 2048u, 8192u}) {
     double *a, *b;
     uint32_t* err;
     CK(cudaMalloc(&a, n * 8)); CK(cudaMalloc(&b, n * 8)); CK(cudaMalloc(&err, 16));
@@ -57,7 +57,7 @@ int main(int argc, char** argv) {
 #ifdef IPLS_BASE_TIMING
     { unsigned long long ph[16]; cudaMemcpyFromSymbol(ph, g_base_phase, sizeof(ph)); unsigned long long z[16] = {0};
       cudaMemcpyToSymbol(g_base_phase, z, sizeof(z)); double tot = 0; for (int q = 0; q < 11; ++q) tot += ph[q];
-      printf("  phases (cycles/window, thread 0 / lane 0):"); for (int q = 0; q < 11; ++q) printf(" %d:%.0f", q, ph[q] / 6.0 / nw); printf("\n"); }
+      printf("  phases (cycles/window, thread 0 / lane 0):"); for (int q = 0; q < 11; ++q) printf(" %d:%.0f", q, ph[q] / 6.0 / nw); printf(" (cycles per window per warp)"); printf("\n"); }
 #endif
     printf("W=%5u windows=%u  %.3f ms  %.0f GB/s (16 B/key)  unsorted=%u\n", W, nw, best, 16.0 * n / best / 1e6, he[2]);
     cudaFree(a); cudaFree(b); cudaFree(err); cudaFree(dw);
