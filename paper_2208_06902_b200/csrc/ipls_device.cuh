@@ -136,6 +136,12 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
       ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// global store that asks the L2 to keep the line (partially written bucket runs stay
+// resident until the next tile completes them)
+__device__ __forceinline__ void st_evict_last(uint64_t* p, uint64_t v) {
+  asm volatile("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+               " st.global.L2::cache_hint.b64 [%0], %1, pol;\n}" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

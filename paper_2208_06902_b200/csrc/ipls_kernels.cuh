@@ -922,7 +922,7 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
           if (stage[q - 1] != v) cflag[b] = 2;
         }
       }
-      reinterpret_cast<uint64_t*>(adj[b])[q] = v;
+      st_evict_last(reinterpret_cast<uint64_t*>(adj[b]) + q, v);
     }
     SC_TICK(4);
     if (__syncthreads_or(bad)) {
