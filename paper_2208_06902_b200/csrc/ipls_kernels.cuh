@@ -15,6 +15,13 @@
 
 namespace ipls {
 
+#ifdef IPLS_SCATTER_TIMING  // dev builds only (tools/phase_scatter.py)
+__device__ unsigned long long g_sc_phase[16];
+#define FIT_TICK(N) do { if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_sc_phase[N], (unsigned long long)(t_ - ft_prev_)); ft_prev_ = t_; } } while (0)
+#else
+#define FIT_TICK(N)
+#endif
+
 constexpr int kCThreads = 512;                 // classify
 constexpr int kCItems = 8;
 constexpr int kCTile = kCThreads * kCItems;    // 4096
@@ -131,7 +138,10 @@ __device__ void block_sort_ok(uint64_t* a, uint64_t* tmp, uint32_t* fh, uint32_t
       run += c;
     }
   }
-  if (__syncthreads_or(mxc > kFineOverflow)) {
+  // sh == 0: every coarse bin is one value, so the counting pass is already an exact sort
+  // (duplicate-heavy samples, e.g. root-dups).  Otherwise bins are finished by insertion
+  // sort, unless one holds more than kFineOverflow keys (then a bitonic sort).
+  if (__syncthreads_or(sh > 0 && mxc > kFineOverflow)) {  // also orders the scan writes
     bitonic_sort_smem<NT>(a, n);
     return;
   }
@@ -141,13 +151,15 @@ __device__ void block_sort_ok(uint64_t* a, uint64_t* tmp, uint32_t* fh, uint32_t
     tmp[pos] = v;
   }
   __syncthreads();
-  for (uint32_t f = threadIdx.x; f < n; f += NT) {
-    uint32_t beg = f ? fh[f - 1] : 0u, end = fh[f];
-    for (uint32_t i = beg + 1; i < end; ++i) {
-      uint64_t x = tmp[i];
-      uint32_t j = i;
-      while (j > beg && tmp[j - 1] > x) { tmp[j] = tmp[j - 1]; --j; }
-      tmp[j] = x;
+  if (sh > 0) {
+    for (uint32_t f = threadIdx.x; f < n; f += NT) {
+      uint32_t beg = f ? fh[f - 1] : 0u, end = fh[f];
+      for (uint32_t i = beg + 1; i < end; ++i) {
+        uint64_t x = tmp[i];
+        uint32_t j = i;
+        while (j > beg && tmp[j - 1] > x) { tmp[j] = tmp[j - 1]; --j; }
+        tmp[j] = x;
+      }
     }
   }
   __syncthreads();
@@ -211,6 +223,9 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
   __shared__ uint64_t s_pivot;
   const SegDesc sg = segs[blockIdx.x];
   const uint32_t S = sg.S;
+#ifdef IPLS_SCATTER_TIMING
+  long long ft_prev_ = clock64();
+#endif
   if (presorted_ok) {
     for (uint32_t j = threadIdx.x; j < S; j += kFitThreads) a[j] = presorted_ok[j];
     __syncthreads();
@@ -225,7 +240,9 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
       a[j] = ok_of<F64>(__ldg(src + idx));
     }
     __syncthreads();
+    FIT_TICK(8);
     block_sort_ok<kFitThreads>(a, tmp, fh, S, ss);
+    FIT_TICK(9);
   }
   if (samples_out)
     for (uint32_t j = threadIdx.x; j < S; j += kFitThreads) samples_out[sg.sample_off + j] = a[j];
@@ -281,6 +298,7 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     md.kind = kModelEq3; md.A = 0.0; md.B = 0.0; md.D = 0; md.capped = 0;
     md.pivot_ok = s_pivot; md.k_eff = 3;
   }
+  FIT_TICK(10);
   if (threadIdx.x == 0) models[blockIdx.x] = md;
 }
 
@@ -774,9 +792,6 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
 // per-bucket pass after the write-out compares that key with the chunk's first key of the
 // bucket.  The chunk's flags (0 empty, 1 one value, 2 several) and values go to global memory
 // for segment_emit.
-#ifdef IPLS_SCATTER_TIMING
-__device__ unsigned long long g_sc_phase[16];
-#endif
 constexpr int kSThreads4 = 1024;
 constexpr int kSWarps4 = kSThreads4 / 32;          // 32
 constexpr int kSRounds4 = 8;                       // keys per thread per tile

@@ -19,12 +19,15 @@ src = torch.from_numpy(a.view(np.int64)).cuda()
 t = torch.empty_like(src)
 lib = ipls.lib()
 ph = (ctypes.c_ulonglong * 16)()
-for rep in range(3):
+for rep in range(2):
     t.copy_(src)
     torch.cuda.synchronize()
     lib.ipls_debug_scatter_phases(ph, 1)
     ipls.sort(t, k=cfg.k, base_case=cfg.base_case, key_type=kt)
     torch.cuda.synchronize()
 lib.ipls_debug_scatter_phases(ph, 1)
+tr = ipls.sort_trace(src.clone(), k=cfg.k, base_case=cfg.base_case, key_type=kt) if False else None
 tiles = sum((int(n) + 8191) // 8192 for n in [a.size]) * 2  # approx: 2 levels over all keys
-print("cycles per tile (thread 0):", " ".join(f"{i}:{ph[i] / tiles:.0f}" for i in range(7)))
+print("scatter cycles per tile (thread 0):", " ".join(f"{i}:{ph[i] / tiles:.0f}" for i in range(7)))
+print("fit cycle sums over all CTAs of the last sort (x1e6): gather", ph[8] / 1e6, "sort", ph[9] / 1e6,
+      "fmcd", ph[10] / 1e6)
