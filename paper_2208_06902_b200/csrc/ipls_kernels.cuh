@@ -33,10 +33,11 @@ constexpr uint32_t kMaxK = 1024;
 constexpr int kWBCap = 256;                      // keys per warp window
 constexpr int kWBBinsPerKey = 2;
 constexpr int kWBBins = kWBBinsPerKey * kWBCap;  // fine bins per warp
-constexpr int kWBWarps = 24;                     // warps per CTA, one CTA per SM
+constexpr int kWBWarps = 30;                     // warps per CTA, one CTA per SM
 constexpr int kWBStride = kWBCap + 4;            // keys per prefetch buffer (+ alignment slack)
-constexpr size_t kWBSmemPerWarp =
-    (size_t)2 * kWBStride * 8 + kWBCap * 8 + kWBCap * 4 + (kWBBins + 32) * 4;
+constexpr int kWBItems = kWBCap / 32;            // keys per lane (held in registers)
+constexpr size_t kWBSmemPerWarp = (size_t)2 * kWBStride * 8 + kWBCap * 4 + (kWBBins + 32) * 4;
+static_assert((kWBBins + 32) * 4 >= kWBCap * 8, "the bins region doubles as the rank buffer");
 constexpr uint32_t kFineOverflow = 32;          // fine-bin load that triggers the bitonic fallback
 
 // ------------------------------------------------------------------------------------
@@ -1361,9 +1362,9 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
   constexpr int BPL = kWBBins / 32;  // bins per lane
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   uint64_t* IN = reinterpret_cast<uint64_t*>(smraw + wp * kWBSmemPerWarp);  // 2 x kWBStride
-  uint64_t* B = IN + 2 * kWBStride;                                          // kWBCap
-  uint32_t* FS = reinterpret_cast<uint32_t*>(B + kWBCap);                    // kWBCap
+  uint32_t* FS = reinterpret_cast<uint32_t*>(IN + 2 * kWBStride);            // kWBCap
   uint32_t* bins = FS + kWBCap;                                              // kWBBins + 32
+  uint64_t* T = reinterpret_cast<uint64_t*>(bins);                           // rank buffer
   uint64_t* mbar = s_mbar[wp];
   const uint32_t gw = blockIdx.x * kWBWarps + wp, gstride = gridDim.x * kWBWarps;
   // lane 0: start the bulk copy of the window described by wv into IN[b].  Descriptors are
@@ -1414,10 +1415,17 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     const WinGeom gm = win_geom(src, len);
     uint64_t* INb = IN + (size_t)b * kWBStride;
     uint64_t* K = INb + 2 - gm.head;  // key i of the window
+    uint64_t* B = INb;                // placement array once the keys are in registers
     if (lane == 0 && gm.head) K[0] = __ldcs(src);
     if (lane == 1 && gm.tail) K[len - 1] = __ldcs(src + len - 1);
     mbar_wait(&mbar[b], (it >> 1) & 1);
     __syncwarp();
+    uint64_t v[kWBItems];
+#pragma unroll
+    for (int j = 0; j < kWBItems; ++j) {
+      const uint32_t i = j * 32 + lane;
+      v[j] = (i < len) ? K[i] : 0ull;
+    }
     WB_TICK(1);
     // ---- bounds ----
     double mn = 0.0, range;
@@ -1425,10 +1433,13 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     if constexpr (F64) {
       double mx = -__longlong_as_double(0x7ff0000000000000ll);
       mn = -mx;
-      for (uint32_t i = lane; i < len; i += 32) {
-        const double x = __longlong_as_double((long long)K[i]);
-        mn = fmin(mn, x);
-        mx = fmax(mx, x);
+#pragma unroll
+      for (int j = 0; j < kWBItems; ++j) {
+        if (j * 32 + lane < len) {
+          const double x = __longlong_as_double((long long)v[j]);
+          mn = fmin(mn, x);
+          mx = fmax(mx, x);
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1437,10 +1448,12 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       }
       range = mx - mn;
     } else {
-      for (uint32_t i = lane; i < len; i += 32) {
-        const uint64_t x = K[i];
-        umn = min(umn, x);
-        umx = max(umx, x);
+#pragma unroll
+      for (int j = 0; j < kWBItems; ++j) {
+        if (j * 32 + lane < len) {
+          umn = min(umn, v[j]);
+          umx = max(umx, v[j]);
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1454,7 +1467,10 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     if (!F64 && umn == umx) {
       // nothing to sort
     } else if (!(range > 0.0) || !(range < 1.79e308)) {  // +-0 mixes, infinities, overflow
-      for (uint32_t i = lane; i < len; i += 32) B[i] = K[i];
+      __syncwarp();  // every lane holds its keys: B may overwrite K
+#pragma unroll
+      for (int j = 0; j < kWBItems; ++j)
+        if (j * 32 + lane < len) B[j * 32 + lane] = v[j];
       __syncwarp();
       warp_bitonic_ok<F64>(B, len, lane);
       OUT = B;
@@ -1465,14 +1481,18 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       // lane-contiguous scan walk is conflict-free.
       for (uint32_t q = lane; q < (uint32_t)(kWBBins + 32); q += 32) bins[q] = 0u;
       __syncwarp();
-      for (uint32_t i = lane; i < len; i += 32) {
-        const uint64_t x = K[i];
-        double y;
-        if constexpr (F64) y = __longlong_as_double((long long)x) - mn;
-        else y = (double)(x - umn);
-        uint32_t fb = min(__double2uint_rz(y * scale), nb - 1);
-        FS[i] = fb;  // unpadded bin
-        atomicAdd(&bins[fb + (fb >> 5)], 1u);
+      uint32_t fr[kWBItems];  // bin, then bin | slot << 16
+#pragma unroll
+      for (int j = 0; j < kWBItems; ++j) {
+        fr[j] = 0;
+        if (j * 32 + lane < len) {
+          double y;
+          if constexpr (F64) y = __longlong_as_double((long long)v[j]) - mn;
+          else y = (double)(v[j] - umn);
+          const uint32_t fb = min(__double2uint_rz(y * scale), nb - 1);
+          fr[j] = fb;
+          atomicAdd(&bins[fb + (fb >> 5)], 1u);
+        }
       }
       __syncwarp();
     WB_TICK(3);
@@ -1503,11 +1523,14 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       const bool overflow = __any_sync(0xffffffffu, mxc > kFineOverflow);
       __syncwarp();
     WB_TICK(4);
-      for (uint32_t i = lane; i < len; i += 32) {
-        const uint32_t fb = FS[i];
-        const uint32_t slot = atomicAdd(&bins[fb + (fb >> 5)], 1u);
-        B[slot] = K[i];
-        FS[i] = fb | (slot << 16);
+#pragma unroll
+      for (int j = 0; j < kWBItems; ++j) {
+        if (j * 32 + lane < len) {
+          const uint32_t fb = fr[j];
+          const uint32_t slot = atomicAdd(&bins[fb + (fb >> 5)], 1u);
+          B[slot] = v[j];
+          fr[j] = fb | (slot << 16);
+        }
       }
       __syncwarp();
     WB_TICK(5);
@@ -1516,16 +1539,17 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
         OUT = B;
       } else {
         // bins hold bin ends now.  Keys alone in their bin are already in place in B.  Keys
-        // of multi-key bins (a minority) are compacted into a worklist (in place over FS);
-        // each ranks itself among its bin (smaller, or equal at a smaller slot) and is
-        // written to INb (dead input copy) at bin start + rank, then copied back to B.
+        // of multi-key bins (a minority) are compacted into a worklist (FS); each ranks itself
+        // among its bin (smaller, or equal at a smaller slot) and is written to T (the dead
+        // bins region) at bin start + rank, then copied back to B.
         uint32_t nwork = 0;
-        for (uint32_t base = 0; base < len; base += 32) {
-          const uint32_t i = base + lane;
+#pragma unroll
+        for (int jj = 0; jj < kWBItems; ++jj) {
+          const uint32_t i = jj * 32 + lane;
           uint32_t item = 0;
           bool multi = false;
           if (i < len) {
-            const uint32_t w = FS[i];
+            const uint32_t w = fr[jj];
             const uint32_t fb = w & 0xffffu, slot = w >> 16;
             const uint32_t beg = fb ? bins[(fb - 1) + ((fb - 1) >> 5)] : 0u;
             const uint32_t end = bins[fb + (fb >> 5)];
@@ -1547,13 +1571,13 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
             const uint64_t y = B[p];
             r += (p != slot && (key_before<F64>(y, x) || (y == x && p < slot))) ? 1u : 0u;
           }
-          INb[r] = x;
+          T[r] = x;
         }
         __syncwarp();
     WB_TICK(7);
         for (uint32_t j = lane; j < nwork; j += 32) {
           const uint32_t slot = FS[j] & 1023u;
-          B[slot] = INb[slot];
+          B[slot] = T[slot];
         }
         OUT = B;
       }
