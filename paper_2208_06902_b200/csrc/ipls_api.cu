@@ -173,7 +173,8 @@ FixedLayout fixed_layout(const Params& p) {
 // Per-level metadata (sized by the level's actual counts).  `status` comes first so a fresh
 // allocation can be cleared cheaply.
 struct MetaLayout {
-  size_t status, cflag, cref, chunk_pre, models, samples, seg_dst, seg_tot, seg_done, total;
+  size_t status, cflag, cref, chunk_pre, models, samples, seg_dst, seg_tot, seg_done, seg_term,
+      total;
 };
 
 MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_t k) {
@@ -189,6 +190,7 @@ MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_
   L.seg_dst = take(segs * k * 8);
   L.seg_tot = take(segs * k * 4);
   L.seg_done = take(segs * 4);
+  L.seg_term = take(segs * 4);
   L.total = o;
   return L;
 }
@@ -402,6 +404,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     la.cflag = at<uint8_t>(meta, ML.cflag);
     la.cref = at<uint64_t>(meta, ML.cref);
     la.seg_done = at<uint32_t>(meta, ML.seg_done);
+    la.seg_term = at<uint32_t>(meta, ML.seg_term);
     la.chunk_pre = chunk_pre;
     la.seg_dst = seg_dst;
     la.seg_tot = seg_tot;
@@ -738,6 +741,7 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
     la.cflag = at<uint8_t>(meta, ML.cflag);
     la.cref = at<uint64_t>(meta, ML.cref);
     la.seg_done = at<uint32_t>(meta, ML.seg_done);
+    la.seg_term = at<uint32_t>(meta, ML.seg_term);
     la.chunk_pre = at<uint32_t>(meta, ML.chunk_pre);
     la.seg_dst = at<uint64_t>(meta, ML.seg_dst);
     la.seg_tot = at<uint32_t>(meta, ML.seg_tot);

@@ -320,6 +320,7 @@ struct LevelArgs {
   uint8_t* cflag;        // [chunk][k] scatter homogeneity flag: 0 empty, 1 one value, 2 several
   uint64_t* cref;        // [chunk][k] the chunk's value of a one-value bucket
   uint32_t* seg_done;    // [seg]      chunks of the segment scattered so far
+  uint32_t* seg_term;    // [seg]      1: every child <= base case (terminal segment)
   uint32_t epoch;
   uint32_t* err;
   int check_nan;
@@ -513,6 +514,13 @@ __device__ void segment_bases(const LevelArgs& a, uint32_t s, const SegDesc& sg,
     ex += tot[q];
   }
   if (a.single_offsets && threadIdx.x == 0) a.single_offsets[md.k_eff] = sg.m;
+  // Terminal segment: every child goes to the base case, so the order inside a child before
+  // the base case is unobservable (R13) and the scatter may place it unstably.
+  int big = 0;
+#pragma unroll
+  for (int q = 0; q < kCBpt; ++q) big |= tot[q] > a.base_case;
+  const int any_big = __syncthreads_or(big);
+  if (threadIdx.x == 0) a.seg_term[s] = (!a.single_offsets && !any_big) ? 1u : 0u;
 }
 
 // Per segment, after its last chunk has been scattered (run by that CTA): child classes with
@@ -983,6 +991,97 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
   }
 }
 
+
+// Terminal segments (every child <= base case): the children are sorted by the base case
+// right after this level, so the scatter does not need stable ranks.  Per tile: bucket counts
+// (smem atomics), a scan over buckets, placement by an atomic cursor per bucket, write-out as
+// in the stable path.  No per-warp counters, no cross-warp scan, no stability check; no
+// homogeneity tracking either (only children above the base case can be homogeneous-final).
+template <bool F64, bool EQ3>
+__device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict__ dst_user,
+                                       uint64_t* __restrict__ dst_scr, uint32_t c,
+                                       const ChunkDesc& ch, const ModelDev& md,
+                                       unsigned char* smraw) {
+  constexpr int NT = kSThreads4;
+  const uint32_t k = a.k;
+  uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);          // kSTile4
+  uint64_t* runa = stage + kSTile4;                               // k
+  uint64_t* adj = runa + k;                                       // k
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(adj + k);           // k
+  uint32_t* cur = cnt + k;                                        // k
+  uint16_t* sbk = reinterpret_cast<uint16_t*>(cur + k);           // kSTile4
+  __shared__ uint32_t s_warp[40];
+  const Bucketer<F64, EQ3> bucket(md, k);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  for (uint32_t b = threadIdx.x; b < k; b += NT) {
+    const uint64_t d = a.seg_dst[(size_t)ch.seg * k + b] + a.chunk_pre[(size_t)c * k + b];
+    uint64_t* buf = (d & kDstUserBit) ? dst_user : dst_scr;
+    runa[b] = reinterpret_cast<uint64_t>(buf + (d & ~kDstUserBit));
+  }
+  const uint64_t* p = a.src + ch.start;
+  uint64_t key[kSRounds4];
+#pragma unroll
+  for (int r = 0; r < kSRounds4; ++r) {
+    const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
+    key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
+  }
+  for (uint32_t t0 = 0; t0 < ch.len; t0 += kSTile4) {
+    const uint32_t tl = min((uint32_t)kSTile4, ch.len - t0);
+    for (uint32_t b = threadIdx.x; b < k; b += NT) cnt[b] = 0u;
+    __syncthreads();
+    uint32_t bk[kSRounds4];
+#pragma unroll
+    for (int r = 0; r < kSRounds4; ++r) {
+      const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
+      bk[r] = 0xffffu;
+      if (i < tl) {
+        bk[r] = bucket(key[r]);
+        atomicAdd(&cnt[bk[r]], 1u);
+      }
+    }
+    __syncthreads();
+    {
+      uint32_t cc[kSBpt], sum = 0;
+#pragma unroll
+      for (int q = 0; q < kSBpt; ++q) {
+        const uint32_t b = threadIdx.x * kSBpt + q;
+        cc[q] = (b < k) ? cnt[b] : 0u;
+        sum += cc[q];
+      }
+      uint32_t ex = block_exclusive_scan<NT>(sum, s_warp, nullptr);
+#pragma unroll
+      for (int q = 0; q < kSBpt; ++q) {
+        const uint32_t b = threadIdx.x * kSBpt + q;
+        if (b < k) {
+          cur[b] = ex;
+          const uint64_t ra = runa[b];
+          adj[b] = ra - 8ull * ex;
+          runa[b] = ra + 8ull * cc[q];
+        }
+        ex += cc[q];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kSRounds4; ++r) {
+      if (bk[r] != 0xffffu) {
+        const uint32_t pos = atomicAdd(&cur[bk[r]], 1u);
+        stage[pos] = key[r];
+        sbk[pos] = (uint16_t)bk[r];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kSRounds4; ++r) {  // prefetch the next tile while this one drains
+      const uint32_t i = t0 + kSTile4 + wp * (kSRounds4 * 32) + r * 32 + lane;
+      key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < tl; q += NT)
+      st_evict_last(reinterpret_cast<uint64_t*>(adj[sbk[q]]) + q, stage[q]);
+    __syncthreads();
+  }
+}
+
 template <bool F64>
 __global__ __launch_bounds__(kSThreads4, 1) void k_scatter(LevelArgs a, uint64_t* __restrict__ dst_user,
                                                            uint64_t* __restrict__ dst_scr) {
@@ -993,10 +1092,17 @@ __global__ __launch_bounds__(kSThreads4, 1) void k_scatter(LevelArgs a, uint64_t
   const uint32_t c = blockIdx.x;
   const ChunkDesc ch = a.chunks[c];
   const ModelDev md = a.models[ch.seg];
-  if (md.kind == kModelEq3)
+  const bool terminal = !a.single_offsets && a.seg_term[ch.seg];
+  if (terminal) {
+    if (md.kind == kModelEq3)
+      scatter_chunk_unstable<F64, true>(a, dst_user, dst_scr, c, ch, md, smraw);
+    else
+      scatter_chunk_unstable<F64, false>(a, dst_user, dst_scr, c, ch, md, smraw);
+  } else if (md.kind == kModelEq3) {
     scatter_chunk<F64, true>(a, dst_user, dst_scr, c, ch, md, smraw);
-  else
+  } else {
     scatter_chunk<F64, false>(a, dst_user, dst_scr, c, ch, md, smraw);
+  }
   if (a.single_offsets) return;  // ipls_partition_level: no next level
   const SegDesc sg = a.segs[ch.seg];
   __threadfence();

@@ -166,9 +166,24 @@ def test_sort_parity_fuzz(ipls, kind, size):
                           snapshot_levels=max(1, ores.levels))
     assert host(t, a.dtype).tobytes() == want.tobytes()
     compare_traces(gtr, ores)
+    # Layout after every level: bit-exact, except inside the children of terminal segments
+    # (every child <= base case).  Those are handed to the base case, an exact sort, right
+    # after the level, so their interior order is unspecified (R11); the GPU places
+    # them unstably and only their multisets must agree.
+    free = []  # (level, begin, end) of children whose interior order is unspecified
+    for o in ores.records:
+        cnt = np.asarray(o.counts, dtype=np.int64)
+        if cnt.max() <= B:
+            edges = o.begin + np.concatenate([[0], np.cumsum(cnt)])
+            free += [(o.level, int(lo), int(hi)) for lo, hi in zip(edges[:-1], edges[1:]) if hi - lo > 1]
     for lv in range(ores.levels):
-        assert np.array_equal(gtr.snapshots[lv].cpu().numpy().view(np.uint64),
-                              ores.snapshots[lv]), f"layout after level {lv} differs"
+        g = gtr.snapshots[lv].cpu().numpy().view(np.uint64).copy()
+        w = ores.snapshots[lv].copy()
+        for flv, lo, hi in free:
+            if flv <= lv:
+                g[lo:hi] = np.sort(g[lo:hi])
+                w[lo:hi] = np.sort(w[lo:hi])
+        assert np.array_equal(g, w), f"layout after level {lv} differs"
 
 
 def test_worked_example_sort(ipls, golden):
