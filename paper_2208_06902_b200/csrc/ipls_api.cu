@@ -287,6 +287,8 @@ void set_attrs() {
   if (done) return;
   ck(cudaFuncSetAttribute(k_gather_fit<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)fit_smem(kFitMaxS)));
+  ck(cudaFuncSetAttribute(k_fit_small<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)kFSSmem));
   ck(cudaFuncSetAttribute(k_base_sort<F64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)base_smem()));
   ck(cudaFuncSetAttribute(k_base_sort<F64, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -392,8 +394,12 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     {
       IPLS_PROF("gather_fit", 0);
       const uint32_t cap = fit_cap(max_S);
+      uint32_t* redo = at<uint32_t>(meta, ML.seg_term);  // scratch until K2 writes seg_term
+      k_fit_small<F64><<<nseg, kFSThreads, kFSSmem, st>>>(src, segs, seed, level, k,
+                                                          trace ? samples : nullptr, models, redo);
+      ck_launch();
       k_gather_fit<F64><<<nseg, kFitThreads, fit_smem(cap), st>>>(
-          src, segs, seed, level, k, cap, trace ? samples : nullptr, models, nullptr);
+          src, segs, seed, level, k, cap, trace ? samples : nullptr, models, nullptr, redo);
       ck_launch();
     }
     LevelArgs la{};
@@ -668,11 +674,11 @@ ipls_status ipls_fit_fmcd(const void* d_sorted_sample, size_t S, ipls_key_type t
     if (t == IPLS_KEY_F64) {
       set_attrs<true>();
       k_gather_fit<true><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, k, cap,
-                                                                nullptr, dmod, smp);
+                                                                nullptr, dmod, smp, nullptr);
     } else {
       set_attrs<false>();
       k_gather_fit<false><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, k, cap,
-                                                                 nullptr, dmod, smp);
+                                                                 nullptr, dmod, smp, nullptr);
     }
     ck_launch();
     ModelDev hm;

@@ -215,7 +215,9 @@ template <bool F64>
 __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
     uint32_t level, uint32_t k, uint32_t cap, uint64_t* __restrict__ samples_out,
-    ModelDev* __restrict__ models, const uint64_t* __restrict__ presorted_ok) {
+    ModelDev* __restrict__ models, const uint64_t* __restrict__ presorted_ok,
+    const uint32_t* __restrict__ redo) {
+  if (redo && !redo[blockIdx.x]) return;  // fitted by k_fit_small
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* a = reinterpret_cast<uint64_t*>(smraw);   // cap
   uint64_t* tmp = a + cap;                             // cap
@@ -300,6 +302,202 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     md.pivot_ok = s_pivot; md.k_eff = 3;
   }
   FIT_TICK(10);
+  if (threadIdx.x == 0) models[blockIdx.x] = md;
+}
+
+
+// Phases 1-3 for segments with S <= kFSMax samples: 256 threads, samples held in registers,
+// 3 CTAs per SM (the 1024-thread k_gather_fit below takes S > kFSMax, i.e. level 0 at 1e8
+// keys, and any segment whose sample overflows a fine bin; the flag redo[s] tells which).
+// Same result as k_gather_fit: same sample, exact sort, Listing 1 by galloping + bisection.
+constexpr int kFSThreads = 256;
+constexpr int kFSItems = 20;                     // samples per thread
+constexpr int kFSMax = kFSThreads * kFSItems;    // 5120 (S(m) for m <= 2^25 at k = 1024)
+constexpr size_t kFSSmem = (size_t)kFSMax * 12;
+
+template <bool F64>
+__global__ __launch_bounds__(kFSThreads, 3) void k_fit_small(
+    const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
+    uint32_t level, uint32_t k, uint64_t* __restrict__ samples_out, ModelDev* __restrict__ models,
+    uint32_t* __restrict__ redo) {
+  constexpr int NT = kFSThreads, NW = NT / 32, IT = kFSItems;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* B = reinterpret_cast<uint64_t*>(smraw);      // kFSMax
+  uint32_t* fh = reinterpret_cast<uint32_t*>(B + kFSMax);  // kFSMax
+  __shared__ SortSmem ss;
+  __shared__ uint64_t s_pivot;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const SegDesc sg = segs[blockIdx.x];
+  const uint32_t S = sg.S;
+  if (S > (uint32_t)kFSMax) {
+    if (threadIdx.x == 0) redo[blockIdx.x] = 1u;
+    return;
+  }
+  // ---- stratified sample (R2, R18), as ordering keys in registers ----
+  const uint64_t t = sm64(sm64(sm64(seed) ^ (uint64_t)level) ^ sg.begin);
+  const uint64_t m = sg.m;
+  uint64_t v[IT];
+  uint64_t mn = ~0ull, mx = 0ull;
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    const uint32_t j = r * NT + threadIdx.x;
+    v[r] = 0;
+    if (j < S) {
+      const uint64_t lo = ((uint64_t)j * m) / S;
+      const uint64_t hi = ((uint64_t)(j + 1) * m) / S;
+      const uint64_t idx = sg.begin + lo + __umul64hi(sm64(t ^ (uint64_t)j), hi - lo);
+      v[r] = ok_of<F64>(__ldg(src + idx));
+      mn = min(mn, v[r]);
+      mx = max(mx, v[r]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) { ss.red[wp] = mn; ss.red[32 + wp] = mx; }
+  for (uint32_t c = threadIdx.x; c < 256; c += NT) ss.ccnt[c] = 0u;
+  {
+    uint4* f4 = reinterpret_cast<uint4*>(fh) + threadIdx.x * (IT / 4);
+#pragma unroll
+    for (int q = 0; q < IT / 4; ++q) f4[q] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  mn = ss.red[0]; mx = ss.red[32];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) { mn = min(mn, ss.red[w]); mx = max(mx, ss.red[32 + w]); }
+  // ---- exact sort: coarse + fine interpolation bins, counting placement, in-bin insertion ----
+  if (mn == mx) {
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      const uint32_t j = r * NT + threadIdx.x;
+      if (j < S) B[j] = v[r];
+    }
+  } else {
+    const int bl = 64 - __clzll((long long)(mx - mn));
+    const int sh = bl > 8 ? bl - 8 : 0;
+#pragma unroll
+    for (int r = 0; r < IT; ++r)
+      if (r * NT + threadIdx.x < S) atomicAdd(&ss.ccnt[(uint32_t)((v[r] - mn) >> sh)], 1u);
+    __syncthreads();
+    {
+      const uint32_t cc = ss.ccnt[threadIdx.x];  // NT == 256 coarse bins
+      const uint32_t ex = block_exclusive_scan<NT>(cc, ss.warp, nullptr);
+      ss.coff[threadIdx.x] = ex;
+    }
+    __syncthreads();
+    uint32_t f[IT];
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      f[r] = 0;
+      if (r * NT + threadIdx.x < S) {
+        f[r] = fine_bin(v[r], mn, sh, ss.coff, ss.ccnt);
+        atomicAdd(&fh[f[r]], 1u);
+      }
+    }
+    __syncthreads();
+    uint32_t mxc = 0;
+    {
+      uint4* f4 = reinterpret_cast<uint4*>(fh) + threadIdx.x * (IT / 4);
+      uint32_t sum = 0;
+#pragma unroll
+      for (int q = 0; q < IT / 4; ++q) {
+        const uint4 c = f4[q];
+        sum += c.x + c.y + c.z + c.w;
+        mxc = max(mxc, max(max(c.x, c.y), max(c.z, c.w)));
+      }
+      uint32_t run = block_exclusive_scan<NT>(sum, ss.warp, nullptr);
+#pragma unroll
+      for (int q = 0; q < IT / 4; ++q) {
+        const uint4 c = f4[q];
+        uint4 o;
+        o.x = run; run += c.x;
+        o.y = run; run += c.y;
+        o.z = run; run += c.z;
+        o.w = run; run += c.w;
+        f4[q] = o;
+      }
+    }
+    // sh == 0: every coarse bin is one value, the counting pass is exact
+    if (__syncthreads_or(sh > 0 && mxc > kFineOverflow)) {
+      if (threadIdx.x == 0) redo[blockIdx.x] = 1u;  // the 1024-thread kernel sorts it
+      return;
+    }
+#pragma unroll
+    for (int r = 0; r < IT; ++r)
+      if (r * NT + threadIdx.x < S) B[atomicAdd(&fh[f[r]], 1u)] = v[r];
+    __syncthreads();
+    if (sh > 0) {
+      const uint32_t f0 = threadIdx.x * IT;
+      const uint32_t beg = f0 ? fh[f0 - 1] : 0u, end = fh[f0 + IT - 1];
+      for (uint32_t i = beg + 1; i < end; ++i) {
+        const uint64_t x = B[i];
+        uint64_t y = B[i - 1];
+        if (y <= x) continue;
+        uint32_t j = i;
+        do { B[j] = y; --j; } while (j > beg && (y = B[j - 1]) > x);
+        B[j] = x;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) redo[blockIdx.x] = 0u;
+  if (samples_out)
+    for (uint32_t j = threadIdx.x; j < S; j += NT) samples_out[sg.sample_off + j] = B[j];
+  if (threadIdx.x == 0) s_pivot = B[S / 2];
+  __syncthreads();
+  // ---- FMCD (Listing 1) on the sorted model values ----
+  ModelDev md{};
+  md.k_eff = k;
+  bool eq3 = (sg.flags & kSegForceEq3) || S < 4;
+  if (!eq3) {
+    double* s = reinterpret_cast<double*>(B);
+    for (uint32_t i = threadIdx.x; i < S; i += NT) s[i] = value_of<F64>(bits_of_ok<F64>(B[i]));
+    __syncthreads();
+    const uint32_t N = S;
+    const uint32_t Dcap = N / 3;
+    const double km2 = (double)(k - 2);
+    uint32_t lo = 0, hi = 0;
+    uint32_t D = 1;
+    bool found = false;
+    while (true) {
+      if (D > Dcap) D = Dcap;
+      if (fmcd_pred<NT>(s, N, D, fmcd_u(s, N, D, km2))) { hi = D; found = true; break; }
+      lo = D;
+      if (D == Dcap) break;
+      D <<= 1;
+    }
+    uint32_t Dres;
+    double ures;
+    if (!found) {
+      Dres = Dcap + 1;
+      ures = fmcd_u(s, N, Dcap, km2);
+      md.capped = 1;
+    } else {
+      while (hi - lo > 1) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (fmcd_pred<NT>(s, N, mid, fmcd_u(s, N, mid, km2))) hi = mid; else lo = mid;
+      }
+      Dres = hi;
+      ures = fmcd_u(s, N, hi, km2);
+      md.capped = 0;
+    }
+    const double A = __ddiv_rn(1.0, ures);
+    const double sum = __dadd_rn(s[N - 1 - Dres], s[Dres]);
+    const double prod = __dmul_rn(A, sum);
+    const double Bm = __ddiv_rn(__dsub_rn((double)k, prod), 2.0);
+    const bool degenerate = !(ures > 0.0) || !isfinite(A) || !isfinite(Bm) || !(A > 0.0);
+    if (!degenerate) {
+      md.kind = kModelLinear; md.A = A; md.B = Bm; md.D = Dres; md.pivot_ok = 0;
+    } else {
+      eq3 = true;
+    }
+  }
+  if (eq3) {
+    md.kind = kModelEq3; md.A = 0.0; md.B = 0.0; md.D = 0; md.capped = 0;
+    md.pivot_ok = s_pivot; md.k_eff = 3;
+  }
   if (threadIdx.x == 0) models[blockIdx.x] = md;
 }
 
