@@ -134,7 +134,7 @@ Params make_params(uint64_t n, uint32_t k, uint32_t B) {
   // together, runs are cut by breakers (<= n / (kWBCap + 1) big base children and <= segs
   // partition/homogeneous children per level) and by segment ends
   uint64_t wins = std::min<uint64_t>(n + 1, 2 * n / kWBCap + 2 * (n / (kWBCap + 1)) + 4 * segs) + 64;
-  uint64_t wbig = std::min<uint64_t>(n / (kWBCap + 1), 2 * n / kBaseMax + 2 * (n / (kWBCap + 1)) + 4 * segs) + 64;
+  uint64_t wbig = std::min<uint64_t>(n / (kWBCap + 1), 2 * n / kBigCap + 2 * (n / (kWBCap + 1)) + 4 * segs) + 64;
   uint64_t fills = n / ((uint64_t)B + 1) + 16;
   p.cap_segs = (uint32_t)segs;
   p.cap_chunks = (uint32_t)chunks;
@@ -264,7 +264,7 @@ void launch_scatter(uint32_t nchunk, cudaStream_t st, const LevelArgs& la, uint6
 }
 size_t classify_smem(uint32_t k) { return (size_t)k * 4; }
 size_t warp_base_smem() { return kWBSmemPerWarp * kWBWarps; }
-size_t base_smem() { return (size_t)2 * kPBStride * 8 + (size_t)kBaseMax * 12; }
+size_t base_smem() { return kBCSmem; }
 int g_num_sms = 0;
 uint32_t num_sms() {
   if (!g_num_sms) {
@@ -330,9 +330,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     ck(cudaMemcpyAsync(dw, &w, sizeof(Window), cudaMemcpyHostToDevice, st));
     {
       IPLS_PROF("base_sort", 16.0 * n);
-      uint32_t* tk = at<uint32_t>(fixed, FL.tickets);
-      ck(cudaMemsetAsync(tk, 0, 4, st));
-      k_base_sort<F64, F64><<<1, kPBThreads, base_smem(), st>>>(dw, 1, tk, keys, scr, d_err);
+      k_base_sort<F64, F64><<<1, kBCThreads, base_smem(), st>>>(dw, keys, scr, d_err);
       ck_launch();
     }
     ck(cudaMemcpyAsync(&h_ctr[1].err, d_err, 4, cudaMemcpyDeviceToHost, st));
@@ -489,10 +487,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     }
     if (c.n_wbig) {
       IPLS_PROF("base_sort", 16.0 * c.wbig_keys);
-      uint32_t* tk = at<uint32_t>(fixed, FL.tickets);
-      ck(cudaMemsetAsync(tk, 0, 4, st));
-      k_base_sort<F64, false><<<std::min(c.n_wbig, num_sms()), kPBThreads, base_smem(), st>>>(
-          wbig, c.n_wbig, tk, keys, scr, d_err);
+      k_base_sort<F64, false><<<c.n_wbig, kBCThreads, base_smem(), st>>>(wbig, keys, scr, d_err);
       ck_launch();
     }
     if (c.n_fills) {

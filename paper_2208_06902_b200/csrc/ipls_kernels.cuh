@@ -29,6 +29,12 @@ constexpr int kFitThreads = 1024;
 constexpr int kFitMaxS = 8192;
 constexpr int kBaseMax = 8192;                 // keys per base-case window (W + B)
 constexpr uint32_t kMaxK = 1024;
+// big-window base case (k_base_sort)
+constexpr int kBCThreads = 512;
+constexpr int kBCItems = 8;
+constexpr int kBigCap = kBCThreads * kBCItems;  // 4096 = the largest base child
+constexpr size_t kBCSmem = (size_t)kBigCap * 8 * 2 + (size_t)kBigCap * 4;
+
 // small-window base case (k_base_warp)
 constexpr int kWBCap = 256;                      // keys per warp window
 constexpr int kWBBinsPerKey = 2;
@@ -838,7 +844,7 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
     }
     pack_windows<NT>(a, sg, k, bb, base, tot, small, (uint32_t)kWBCap, dstbuf, os, wsm, a.wins,
                  a.cap_wins, &a.nctr->n_windows, &a.nctr->win_keys);
-    pack_windows<NT>(a, sg, k, bb, base, tot, bigb, (uint32_t)kBaseMax, dstbuf, os, wsm, a.wins_big,
+    pack_windows<NT>(a, sg, k, bb, base, tot, bigb, (uint32_t)kBigCap, dstbuf, os, wsm, a.wins_big,
                  a.cap_wbig, &a.nctr->n_wbig, &a.nctr->wbig_keys);
   }
   // ---- homogeneous children that land in scratch must be filled into the user array ----
@@ -1332,13 +1338,10 @@ __global__ __launch_bounds__(kSThreads4, 1) void k_scatter(LevelArgs a, uint64_t
 // by bin; every thread then insertion-sorts the contiguous range of its 8 fine bins (keys of
 // different bins are already ordered, so only in-bin inversions move).  Windows whose fine
 // bins overflow (> kFineOverflow keys: adversarial clusters) take a bitonic sort.
-constexpr int kPBThreads = 1024;
-constexpr int kPBItems = kBaseMax / kPBThreads;  // 8
-constexpr int kPBStride = kBaseMax + 4;          // keys per smem buffer (+ alignment slack)
 
 struct BaseSmem {
   uint32_t cinfo[256];   // coarse bin: first fine bin | count << 16
-  uint64_t red[2 * (kPBThreads / 32)];  // per-warp min, then per-warp max
+  uint64_t red[64];      // per-warp min, then per-warp max (<= 32 warps)
   uint32_t warp[40];
   uint64_t mbar[2];
   uint32_t win[2];
@@ -1511,97 +1514,47 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
   return B2;
 }
 
+// One window of big base children (<= kBigCap keys) per CTA: 512 threads, 8 keys per thread
+// in registers, 2 CTAs per SM (80 KB smem each), so one CTA's barriers and load latency
+// overlap the other's work.
+
 template <bool F64, bool NANCHK>
-__global__ __launch_bounds__(kPBThreads, 1) void k_base_sort(
-    const Window* __restrict__ wins, uint32_t nwin, uint32_t* __restrict__ ticket,
-    uint64_t* __restrict__ user, const uint64_t* __restrict__ scr, uint32_t* __restrict__ err) {
-  constexpr int NT = kPBThreads, ITEMS = kPBItems;
+__global__ __launch_bounds__(kBCThreads, 2) void k_base_sort(
+    const Window* __restrict__ wins, uint64_t* __restrict__ user, const uint64_t* __restrict__ scr,
+    uint32_t* __restrict__ err) {
+  constexpr int NT = kBCThreads, ITEMS = kBCItems;
   extern __shared__ __align__(128) unsigned char smraw[];
-  uint64_t* A0 = reinterpret_cast<uint64_t*>(smraw);           // 2 x kPBStride (window buffers)
-  uint64_t* B2 = A0 + 2 * kPBStride;                            // kBaseMax
-  uint32_t* fh = reinterpret_cast<uint32_t*>(B2 + kBaseMax);    // kBaseMax
+  uint64_t* A = reinterpret_cast<uint64_t*>(smraw);           // kBigCap: placement array
+  uint64_t* B2 = A + kBigCap;                                  // kBigCap
+  uint32_t* fh = reinterpret_cast<uint32_t*>(B2 + kBigCap);    // kBigCap
   __shared__ BaseSmem ss;
-  long long t_prev_ = clock64();
-  uint64_t hk = 0, tk = 0;  // thread 0: head/tail keys of the window being prefetched
-  auto issue = [&](uint32_t w, int b) {  // thread 0: start the bulk copy of window w into buffer b
-    const Window wv = wins[w];
-    const uint64_t* g = (wv.buf ? scr : user) + wv.begin;
-    const WinGeom gm = win_geom(g, wv.len);
-    if (gm.body) {
-      mbar_arrive_tx(&ss.mbar[b], gm.body * 8u);
-      bulk_g2s(A0 + (size_t)b * kPBStride + 2, g + gm.head, gm.body * 8u, &ss.mbar[b]);
-    } else {
-      mbar_arrive(&ss.mbar[b]);
-    }
-    if (gm.head) hk = __ldcs(g);
-    if (gm.tail) tk = __ldcs(g + wv.len - 1);
-  };
-  auto place_ends = [&](uint32_t w, int b) {  // thread 0: store head/tail keys beside the body
-    const Window wv = wins[w];
-    const uint64_t* g = (wv.buf ? scr : user) + wv.begin;
-    const WinGeom gm = win_geom(g, wv.len);
-    uint64_t* A = A0 + (size_t)b * kPBStride;
-    if (gm.head) A[1] = hk;
-    if (gm.tail) A[2 + gm.body] = tk;
-  };
-  if (threadIdx.x == 0) {
-    mbar_init(&ss.mbar[0], 1);
-    mbar_init(&ss.mbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const uint32_t w = atomicAdd(ticket, 1u);
-    ss.win[0] = w;
-    if (w < nwin) { issue(w, 0); place_ends(w, 0); }
+  long long t_prev_ = 0;
+  const Window wv = wins[blockIdx.x];
+  const uint32_t len = wv.len;
+  if (len == 0) return;
+  const uint64_t* g = (wv.buf ? scr : user) + wv.begin;
+  uint64_t* dst = user + wv.begin;
+  uint64_t v[ITEMS];
+  bool nan_seen = false;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t i = j * NT + threadIdx.x;
+    const uint64_t bits = (i < len) ? __ldcs(g + i) : 0ull;
+    if (F64 && NANCHK) nan_seen |= isnan(__longlong_as_double((long long)bits));
+    v[j] = ok_of<F64>(bits);
   }
-  __syncthreads();
-  for (uint32_t it = 0;; ++it) {
-    const int b = it & 1;
-    const uint32_t cur = ss.win[b];
-    if (cur >= nwin) break;
-    uint32_t nxt = 0;
-    if (threadIdx.x == 0) {
-      nxt = atomicAdd(ticket, 1u);
-      ss.win[b ^ 1] = nxt;
-      if (nxt < nwin) issue(nxt, b ^ 1);
+  if (NANCHK) {
+    if (__syncthreads_or(nan_seen)) {
+      if (threadIdx.x == 0) atomicOr(err, kErrNan);
+      return;  // the array is left untouched
     }
-    const Window wv = wins[cur];
-    const uint64_t* g = (wv.buf ? scr : user) + wv.begin;
-    uint64_t* dst = user + wv.begin;
-    const uint32_t len = wv.len;
-    const WinGeom gm = win_geom(g, len);
-    uint64_t* A = A0 + (size_t)b * kPBStride;
-    const uint64_t* K = A + 2 - gm.head;  // key i of the window
-  BASE_TICK(0);
-    mbar_wait(&ss.mbar[b], (it >> 1) & 1);
-  BASE_TICK(1);
-    uint64_t v[ITEMS];
-    bool nan_seen = false;
+  }
+  uint64_t mn;
+  const uint64_t* out = sort_regs_to_smem<NT, ITEMS>(v, len, A, B2, fh, ss, mn, t_prev_);
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      const uint32_t i = j * NT + threadIdx.x;
-      const uint64_t bits = (i < len) ? K[i] : 0ull;
-      if (F64 && NANCHK) nan_seen |= isnan(__longlong_as_double((long long)bits));
-      v[j] = ok_of<F64>(bits);
-    }
-    if (NANCHK) {
-      if (__syncthreads_or(nan_seen)) {
-        if (threadIdx.x == 0) atomicOr(err, kErrNan);
-        break;  // block-uniform; the array is left untouched
-      }
-    } else {
-      __syncthreads();  // A is free: it becomes the placement array
-    }
-    uint64_t mn;
-    const uint64_t* out = sort_regs_to_smem<NT, ITEMS>(v, len, A, B2, fh, ss, mn, t_prev_);
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      const uint32_t i = j * NT + threadIdx.x;
-      if (i < len) __stcs(dst + i, bits_of_ok<F64>(out[i] + mn));
-    }
-  BASE_TICK(9);
-    if (threadIdx.x == 0 && nxt < nwin) place_ends(nxt, b ^ 1);
-    fence_proxy_async_smem();  // generic accesses to A before the next bulk copy into it
-    __syncthreads();
-  BASE_TICK(10);
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t i = j * NT + threadIdx.x;
+    if (i < len) __stcs(dst + i, bits_of_ok<F64>(out[i] + mn));
   }
 }
 

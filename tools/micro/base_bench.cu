@@ -25,7 +25,7 @@ __global__ void chk(const double* a, uint64_t n, uint32_t* bad) {
 
 int main(int argc, char** argv) {
   const uint64_t n = 100000000ull;
-  for (uint32_t W : {200u, 256u, 2048u, 8192u}) {
+  for (uint32_t W : {256u, 1024u, 2048u, 4096u}) {
     double *a, *b;
     uint32_t* err;
     CK(cudaMalloc(&a, n * 8)); CK(cudaMalloc(&b, n * 8)); CK(cudaMalloc(&err, 16));
@@ -35,8 +35,7 @@ int main(int argc, char** argv) {
     for (uint32_t w = 0; w < nw; ++w) { hw[w].begin = (uint64_t)w * W; hw[w].len = (uint32_t)std::min<uint64_t>(W, n - hw[w].begin); hw[w].buf = 1; }
     Window* dw; CK(cudaMalloc(&dw, nw * sizeof(Window)));
     CK(cudaMemcpy(dw, hw.data(), nw * sizeof(Window), cudaMemcpyHostToDevice));
-    const int smem = 2 * kPBStride * 8 + kBaseMax * 12;
-    CK(cudaFuncSetAttribute(k_base_sort<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_base_sort<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBCSmem));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     float best = 1e9;
     for (int r = 0; r < 5; ++r) {
@@ -47,7 +46,7 @@ int main(int argc, char** argv) {
         cudaFuncSetAttribute(k_base_warp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws);
         k_base_warp<true><<<148, kWBWarps * 32, ws>>>(dw, nw, (uint64_t*)b, (const uint64_t*)a);
       } else {
-        k_base_sort<true, false><<<148, kPBThreads, smem>>>(dw, nw, err, (uint64_t*)b, (const uint64_t*)a, err + 1);
+        k_base_sort<true, false><<<nw, kBCThreads, kBCSmem>>>(dw, (uint64_t*)b, (const uint64_t*)a, err + 1);
       }
       cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
       float ms; cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms);
