@@ -27,7 +27,6 @@ constexpr int kCItems = 8;
 constexpr int kCTile = kCThreads * kCItems;    // 4096
 constexpr int kFitThreads = 1024;
 constexpr int kFitMaxS = 8192;
-constexpr int kBaseMax = 8192;                 // keys per base-case window (W + B)
 constexpr uint32_t kMaxK = 1024;
 // big-window base case (k_base_sort)
 constexpr int kBCThreads = 512;
@@ -833,7 +832,7 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
   if (stuck) return;  // block-uniform
   // ---- base-case windows ----
   // Base children of <= kWBCap keys ("small") are packed into windows of <= kWBCap keys
-  // (sorted by k_base_warp); base children above kWBCap ("big") into windows of <= kBaseMax
+  // (sorted by k_base_warp); base children above kWBCap ("big") into windows of <= kBigCap
   // keys (k_base_sort).  Every other child breaks a window.
   {
     bool small[BPT], bigb[BPT];
@@ -1343,8 +1342,6 @@ struct BaseSmem {
   uint32_t cinfo[256];   // coarse bin: first fine bin | count << 16
   uint64_t red[64];      // per-warp min, then per-warp max (<= 32 warps)
   uint32_t warp[40];
-  uint64_t mbar[2];
-  uint32_t win[2];
 };
 
 __device__ __forceinline__ uint32_t base_fine_bin(uint64_t d, int sh, const uint32_t* cinfo) {
@@ -1370,7 +1367,7 @@ __device__ __forceinline__ WinGeom win_geom(const uint64_t* g, uint32_t len) {
 
 // Sort the keys v[] (ordering keys; slots j*NT+tid < len valid) of one window.  On return
 // the sorted (ok - min) values are in OUT[0, len) (OUT = B2, or B after the bitonic fallback)
-// and `mn` holds min.  B, B2: kBaseMax u64 smem; fh: kBaseMax u32 smem.  Ends with a barrier.
+// and `mn` holds min.  B, B2: NT*ITEMS u64 smem; fh: NT*ITEMS u32 smem.  Ends with a barrier.
 #ifdef IPLS_BASE_TIMING  // dev harness only: per-phase clock accumulation by thread 0
 __device__ unsigned long long g_base_phase[16];
 #define BASE_TICK(N)                                                         \
