@@ -1,15 +1,17 @@
 // ipls_kernels.cuh — sm_100a kernels of one IPLS distribution level and the base case.
 //
-// Per level (the four phases of P:265-287), three launches:
-//   k_gather_fit      phase 1-3: stratified sample of every segment (R2, R18),
-//                     smem sort of the sample, FMCD fit (Listing 1)
-//   k_classify_scan   phase 4a: model eval + smem histogram per chunk, NaN flag,
-//                     homogeneity (R9), decoupled-lookback prefix of the
-//                     (chunk x bucket) counts; the last chunk of each segment computes the
-//                     bucket bases, child classes (R20), next-level work, base-case windows
-//   k_scatter         phase 4b: stable in-tile rank (smem bitmap multisplit), smem staging by
-//                     bucket, run-contiguous writes (R11)
-// After the level: k_base_sort (base case) and k_fill.
+// Per level (the four phases of P:265-287):
+//   k_fit_small /     phases 1-3: stratified sample of every segment (R2, R18),
+//   k_gather_fit      exact sort of the sample, FMCD fit (Listing 1)
+//   k_classify_scan   phase 4a: model evaluation + smem histogram per chunk, NaN
+//                     flag (level 0), decoupled-lookback prefix of the (chunk x bucket) counts;
+//                     the last chunk of a segment writes the bucket bases (segment_bases)
+//   k_scatter         phase 4b: stable in-tile rank (per-warp atomic counters), or unstable
+//                     placement inside terminal segments; smem staging by bucket, run-contiguous
+//                     writes (R11); homogeneity (R9); the last
+//                     chunk of a segment classes the children (R20) and emits the next level's
+//                     work, the base-case windows and the fills (segment_emit)
+// After the level: k_base_warp / k_base_sort (base case) and k_fill.
 #pragma once
 #include "ipls_device.cuh"
 
