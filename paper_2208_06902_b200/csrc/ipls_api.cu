@@ -259,7 +259,8 @@ struct TraceSink {
 template <bool F64>
 void launch_scatter(uint32_t nchunk, cudaStream_t st, const LevelArgs& la, uint64_t* user,
                     uint64_t* scr) {
-  k_scatter<F64><<<nchunk, kSThreads4, scatter_smem_bytes(la.k), st>>>(la, user, scr);
+  const size_t smem = std::max(scatter_smem_bytes(la.k), scatter_unstable_smem_bytes(la.k));
+  k_scatter<F64><<<nchunk, kSThreads4, smem, st>>>(la, user, scr);
   ck_launch();
 }
 size_t classify_smem(uint32_t k) { return (size_t)k * 4; }
@@ -298,7 +299,8 @@ void set_attrs() {
   ck(cudaFuncSetAttribute(k_classify_scan<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)classify_smem(kMaxK)));
   ck(cudaFuncSetAttribute(k_scatter<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)std::max(scatter_smem_bytes(kMaxK), win_scratch_bytes(kMaxK))));
+                          (int)std::max({scatter_smem_bytes(kMaxK), scatter_unstable_smem_bytes(kMaxK),
+                                         win_scratch_bytes(kMaxK)})));
 
   done = true;
 }

@@ -1202,6 +1202,14 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
 // (smem atomics), a scan over buckets, placement by an atomic cursor per bucket, write-out as
 // in the stable path.  No per-warp counters, no cross-warp scan, no stability check; no
 // homogeneity tracking either (only children above the base case can be homogeneous-final).
+// Tiles are twice as long as the stable path's (16 keys per thread): half the barriers and
+// scans per key, and bucket runs twice as long per tile (fuller L2 lines per write-out).
+constexpr int kURounds = 16;                       // keys per thread per tile
+constexpr int kUTile = kSThreads4 * kURounds;      // 16384
+__host__ __device__ constexpr size_t scatter_unstable_smem_bytes(uint32_t k) {
+  return (size_t)kUTile * 8 + (size_t)k * 8 * 2 + (size_t)k * 4 * 2 + (size_t)kUTile * 2;
+}
+
 template <bool F64, bool EQ3>
 __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict__ dst_user,
                                        uint64_t* __restrict__ dst_scr, uint32_t c,
@@ -1209,12 +1217,12 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
                                        unsigned char* smraw) {
   constexpr int NT = kSThreads4;
   const uint32_t k = a.k;
-  uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);          // kSTile4
-  uint64_t* runa = stage + kSTile4;                               // k
+  uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);          // kUTile
+  uint64_t* runa = stage + kUTile;                                // k
   uint64_t* adj = runa + k;                                       // k
   uint32_t* cnt = reinterpret_cast<uint32_t*>(adj + k);           // k
   uint32_t* cur = cnt + k;                                        // k
-  uint16_t* sbk = reinterpret_cast<uint16_t*>(cur + k);           // kSTile4
+  uint16_t* sbk = reinterpret_cast<uint16_t*>(cur + k);           // kUTile
   __shared__ uint32_t s_warp[40];
   const Bucketer<F64, EQ3> bucket(md, k);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
@@ -1224,25 +1232,27 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
     runa[b] = reinterpret_cast<uint64_t>(buf + (d & ~kDstUserBit));
   }
   const uint64_t* p = a.src + ch.start;
-  uint64_t key[kSRounds4];
+  uint64_t key[kURounds];
 #pragma unroll
-  for (int r = 0; r < kSRounds4; ++r) {
-    const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
+  for (int r = 0; r < kURounds; ++r) {
+    const uint32_t i = wp * (kURounds * 32) + r * 32 + lane;
     key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
   }
-  for (uint32_t t0 = 0; t0 < ch.len; t0 += kSTile4) {
-    const uint32_t tl = min((uint32_t)kSTile4, ch.len - t0);
+  for (uint32_t t0 = 0; t0 < ch.len; t0 += kUTile) {
+    const uint32_t tl = min((uint32_t)kUTile, ch.len - t0);
     for (uint32_t b = threadIdx.x; b < k; b += NT) cnt[b] = 0u;
     __syncthreads();
-    uint32_t bk[kSRounds4];
+    uint32_t bk[kURounds / 2];  // two buckets per word; 0xffff = no key
 #pragma unroll
-    for (int r = 0; r < kSRounds4; ++r) {
-      const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
-      bk[r] = 0xffffu;
+    for (int r = 0; r < kURounds; ++r) {
+      const uint32_t i = wp * (kURounds * 32) + r * 32 + lane;
+      uint32_t bb = 0xffffu;
       if (i < tl) {
-        bk[r] = bucket(key[r]);
-        atomicAdd(&cnt[bk[r]], 1u);
+        bb = bucket(key[r]);
+        atomicAdd(&cnt[bb], 1u);
       }
+      if (r & 1) bk[r >> 1] |= bb << 16;
+      else bk[r >> 1] = bb;
     }
     __syncthreads();
     {
@@ -1268,16 +1278,17 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kSRounds4; ++r) {
-      if (bk[r] != 0xffffu) {
-        const uint32_t pos = atomicAdd(&cur[bk[r]], 1u);
+    for (int r = 0; r < kURounds; ++r) {
+      const uint32_t bb = (bk[r >> 1] >> (16 * (r & 1))) & 0xffffu;
+      if (bb != 0xffffu) {
+        const uint32_t pos = atomicAdd(&cur[bb], 1u);
         stage[pos] = key[r];
-        sbk[pos] = (uint16_t)bk[r];
+        sbk[pos] = (uint16_t)bb;
       }
     }
 #pragma unroll
-    for (int r = 0; r < kSRounds4; ++r) {  // prefetch the next tile while this one drains
-      const uint32_t i = t0 + kSTile4 + wp * (kSRounds4 * 32) + r * 32 + lane;
+    for (int r = 0; r < kURounds; ++r) {  // prefetch the next tile while this one drains
+      const uint32_t i = t0 + kUTile + wp * (kURounds * 32) + r * 32 + lane;
       key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
     }
     __syncthreads();
@@ -1563,28 +1574,18 @@ __global__ __launch_bounds__(kBCThreads, 2) void k_base_sort(
 // TMA bulk copy (mbarrier completion) while it sorts the current one, so every SM keeps
 // ~kWBWarps x 4 KB of loads in flight independently of the sorting work.  Windows are dealt
 // round-robin to the warps of the grid (a contended global ticket per window would
-// serialise at the L2).  Loops over the window are rolled (keys and per-key state live in
-// smem, not in unrolled register arrays) so the kernel stays small in the instruction cache.
+// serialise at the L2).  Each lane holds kWBItems keys of the window in registers.
 //
 // Sort = interpolation sort on the raw keys.  Bin of a key = trunc((x - min) * nb / (max -
 // min)) evaluated in binary64 (f64 keys directly, u64 keys through the exact difference
 // x - min converted to double): every step is monotone, so bins are ordered.  Counting pass
-// into smem, placement, then every key counts the keys of its bin that precede it in
-// ordering-key order (ties by slot) and lands at bin start + that count; the walk length is
-// the largest bin among the 32 lanes (warp-uniform).  Windows whose range is zero or not
-// finite (+-0.0 mixes, infinities, overflow) or whose bins overflow (> kFineOverflow keys:
-// extreme skew) take an exact warp bitonic sort.
-
-// strict "a sorts before b" by ordering key, on raw bits
-template <bool F64>
-__device__ __forceinline__ bool key_before(uint64_t a, uint64_t b) {
-  if constexpr (F64) {
-    const double da = __longlong_as_double((long long)a), db = __longlong_as_double((long long)b);
-    return da < db || (da == db && (long long)a < (long long)b);  // -0.0 before +0.0
-  } else {
-    return a < b;
-  }
-}
+// into smem, placement; keys alone in their bin are then in place, and the keys of multi-key
+// bins (a worklist) count the keys of their bin that precede them (ties by slot) and land at
+// bin start + that count.  Inside a window that does not reach zero all keys have one sign,
+// so raw bits ^ (negative ? 0x7ff..f : 0) compared as u64 is the key order.  Windows that
+// reach zero (they may mix -0.0 and +0.0), whose range is not finite (infinities, overflow)
+// or whose bins overflow (> kFineOverflow keys: extreme skew) take an exact warp bitonic sort
+// on ordering keys.
 
 // exact warp bitonic sort of B[0, len) by ordering key (B has room for the next power of 2)
 template <bool F64>
@@ -1676,40 +1677,45 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     if (lane == 1 && gm.tail) K[len - 1] = __ldcs(src + len - 1);
     mbar_wait(&mbar[b], (it >> 1) & 1);
     __syncwarp();
+    // Slots past the end hold a copy of key 0 so that the bounds need no predicate.
     uint64_t v[kWBItems];
-#pragma unroll
-    for (int j = 0; j < kWBItems; ++j) {
-      const uint32_t i = j * 32 + lane;
-      v[j] = (i < len) ? K[i] : 0ull;
-    }
-    WB_TICK(1);
-    // ---- bounds ----
-    double mn = 0.0, range;
-    uint64_t umn = ~0ull, umx = 0ull;
-    if constexpr (F64) {
-      double mx = -__longlong_as_double(0x7ff0000000000000ll);
-      mn = -mx;
+    {
+      const uint64_t k0 = K[0];
 #pragma unroll
       for (int j = 0; j < kWBItems; ++j) {
-        if (j * 32 + lane < len) {
-          const double x = __longlong_as_double((long long)v[j]);
-          mn = fmin(mn, x);
-          mx = fmax(mx, x);
-        }
+        const uint32_t i = j * 32 + lane;
+        v[j] = (i < len) ? K[i] : k0;
+      }
+    }
+    WB_TICK(1);
+    // ---- bounds (no NaN reaches the base case: R0) ----
+    double mn = 0.0, range;
+    uint64_t umn = v[0], umx = v[0];
+    uint64_t flip = 0;  // ordering of raw bits inside a one-signed window: (bits ^ flip) as u64
+    if constexpr (F64) {
+      double mx = __longlong_as_double((long long)v[0]);
+      mn = mx;
+#pragma unroll
+      for (int j = 1; j < kWBItems; ++j) {
+        const double x = __longlong_as_double((long long)v[j]);
+        mn = x < mn ? x : mn;
+        mx = x > mx ? x : mx;
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const double a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
       }
       range = mx - mn;
+      // a window reaching zero (it may mix -0.0 and +0.0) takes the exact path below
+      if (mn <= 0.0 && mx >= 0.0) range = 0.0;
+      flip = mx < 0.0 ? 0x7fffffffffffffffull : 0ull;
     } else {
 #pragma unroll
-      for (int j = 0; j < kWBItems; ++j) {
-        if (j * 32 + lane < len) {
-          umn = min(umn, v[j]);
-          umx = max(umx, v[j]);
-        }
+      for (int j = 1; j < kWBItems; ++j) {
+        umn = min(umn, v[j]);
+        umx = max(umx, v[j]);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1722,7 +1728,7 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     WB_TICK(2);
     if (!F64 && umn == umx) {
       // nothing to sort
-    } else if (!(range > 0.0) || !(range < 1.79e308)) {  // +-0 mixes, infinities, overflow
+    } else if (!(range > 0.0) || !(range < 1.79e308)) {  // zero inside, infinities, overflow
       __syncwarp();  // every lane holds its keys: B may overwrite K
 #pragma unroll
       for (int j = 0; j < kWBItems; ++j)
@@ -1821,13 +1827,13 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
         for (uint32_t j = lane; j < nwork; j += 32) {
           const uint32_t item = FS[j];
           const uint32_t slot = item & 1023u, beg = (item >> 10) & 1023u, n = item >> 20;
-          const uint64_t x = B[slot];
+          const uint64_t x = B[slot] ^ flip;
           uint32_t r = beg;
           for (uint32_t p = beg; p < beg + n; ++p) {
-            const uint64_t y = B[p];
-            r += (p != slot && (key_before<F64>(y, x) || (y == x && p < slot))) ? 1u : 0u;
+            const uint64_t y = B[p] ^ flip;
+            r += (y < x || (y == x && p < slot)) ? 1u : 0u;
           }
-          T[r] = x;
+          T[r] = x ^ flip;
         }
         __syncwarp();
     WB_TICK(7);
