@@ -113,12 +113,15 @@ struct Params {
   uint32_t cap_segs, cap_chunks, cap_samples, cap_wins, cap_wbig, cap_fills;
 };
 
+#ifndef IPLS_CHUNK_CAP
+#define IPLS_CHUNK_CAP 65536
+#endif
 uint32_t pick_chunk_keys(uint64_t n) {
   // ~8 chunks per SM at level 0 (148 SMs), whole tiles, 4096..65536 keys.
   uint64_t c = n / (148 * 8);
   c = (c + kCTile - 1) / kCTile * kCTile;
   if (c < (uint64_t)kCTile) c = kCTile;
-  if (c > 65536) c = 65536;
+  if (c > IPLS_CHUNK_CAP) c = IPLS_CHUNK_CAP;
   return (uint32_t)c;
 }
 

@@ -1010,7 +1010,7 @@ constexpr int kSThreads4 = 1024;
 constexpr int kSWarps4 = kSThreads4 / 32;          // 32
 constexpr int kSRounds4 = 8;                       // keys per thread per tile
 constexpr int kSBpt = kMaxK / kSThreads4;          // buckets per thread in the scans
-constexpr int kSTile4 = kSThreads4 * kSRounds4;    // 4096
+constexpr int kSTile4 = kSThreads4 * kSRounds4;    // 8192
 constexpr int kSPairs4 = kSWarps4 / 2;             // warp pairs sharing a counter word
 
 __host__ __device__ constexpr size_t scatter_smem_bytes(uint32_t k) {
@@ -1204,7 +1204,10 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
 // homogeneity tracking either (only children above the base case can be homogeneous-final).
 // Tiles are twice as long as the stable path's (16 keys per thread): half the barriers and
 // scans per key, and bucket runs twice as long per tile (fuller L2 lines per write-out).
-constexpr int kURounds = 16;                       // keys per thread per tile
+#ifndef IPLS_UROUNDS
+#define IPLS_UROUNDS 16
+#endif
+constexpr int kURounds = IPLS_UROUNDS;             // keys per thread per tile
 constexpr int kUTile = kSThreads4 * kURounds;      // 16384
 __host__ __device__ constexpr size_t scatter_unstable_smem_bytes(uint32_t k) {
   return (size_t)kUTile * 8 + (size_t)k * 8 * 2 + (size_t)k * 4 * 2 + (size_t)kUTile * 2;

@@ -5,6 +5,8 @@ import numpy as np
 import torch
 import paper_2208_06902_b200 as ipls
 from paper_2208_06902_b200 import datagen
+if os.environ.get("IPLS_LIB"):  # A/B a variant build
+    ipls._LIB_PATH = os.path.abspath(os.environ["IPLS_LIB"])
 
 names = sys.argv[1:] or ["C2"]
 reps = int(os.environ.get("REPS", "8"))
