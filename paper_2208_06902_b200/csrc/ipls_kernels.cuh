@@ -34,17 +34,22 @@ constexpr uint32_t kMaxK = 1024;
 constexpr int kBCThreads = 512;
 constexpr int kBCItems = 8;
 constexpr int kBigCap = kBCThreads * kBCItems;  // 4096 = the largest base child
-constexpr size_t kBCSmem = (size_t)kBigCap * 8 * 2 + (size_t)kBigCap * 4;
+constexpr size_t kBCSmem = (size_t)kBigCap * 8 + (size_t)kBigCap * 4;
 
 // small-window base case (k_base_warp)
 constexpr int kWBCap = 256;                      // keys per warp window
-constexpr int kWBBinsPerKey = 2;
+#ifndef IPLS_WB_BPK
+#define IPLS_WB_BPK 2
+#endif
+#ifndef IPLS_WB_WARPS
+#define IPLS_WB_WARPS 32
+#endif
+constexpr int kWBBinsPerKey = IPLS_WB_BPK;
 constexpr int kWBBins = kWBBinsPerKey * kWBCap;  // fine bins per warp
-constexpr int kWBWarps = 30;                     // warps per CTA, one CTA per SM
+constexpr int kWBWarps = IPLS_WB_WARPS;          // warps per CTA, one CTA per SM
 constexpr int kWBStride = kWBCap + 4;            // keys per prefetch buffer (+ alignment slack)
 constexpr int kWBItems = kWBCap / 32;            // keys per lane (held in registers)
-constexpr size_t kWBSmemPerWarp = (size_t)2 * kWBStride * 8 + kWBCap * 4 + (kWBBins + 32) * 4;
-static_assert((kWBBins + 32) * 4 >= kWBCap * 8, "the bins region doubles as the rank buffer");
+constexpr size_t kWBSmemPerWarp = (size_t)2 * kWBStride * 8 + (size_t)(kWBBins + 32) * 4;
 constexpr uint32_t kFineOverflow = 32;          // fine-bin load that triggers the bitonic fallback
 
 // ------------------------------------------------------------------------------------
@@ -1335,16 +1340,14 @@ __global__ __launch_bounds__(kSThreads4, 1) void k_scatter(LevelArgs a, uint64_t
 }
 
 // ------------------------------------------------------------------------------------
-// Base case: sort windows of whole final segments (<= 8192 keys) by ordering key and
+// Base case: sort windows of whole final segments (<= 4096 keys) by ordering key and
 // write them to the user array.  Buckets are range-ordered (the model is monotone, R7), so
 // sorting a window of consecutive final segments sorts each of them; any exact sort gives the
 // identical bytes (R13).
 //
-// Persistent kernel, one CTA of 1024 threads per SM, windows taken by atomic ticket.  While a
-// window is sorted, the next one streams into the other smem buffer with one TMA bulk copy
-// (cp.async.bulk, mbarrier completion), so DRAM latency is off the critical path.  The keys
-// of the current window move to registers (8 per thread) and their buffer becomes the
-// placement array.
+// Two kernels: k_base_sort (windows of base children above kWBCap keys, one window per
+// 512-thread CTA, keys in registers) and k_base_warp (windows of <= kWBCap keys, one per warp,
+// below).
 //
 // Sort = interpolation sort in ordering-key space: a 256-bin coarse histogram of
 // (ok - min) >> sh gives each coarse bin as many fine bins as it holds keys; the fine bin of
@@ -1382,8 +1385,8 @@ __device__ __forceinline__ WinGeom win_geom(const uint64_t* g, uint32_t len) {
 }
 
 // Sort the keys v[] (ordering keys; slots j*NT+tid < len valid) of one window.  On return
-// the sorted (ok - min) values are in OUT[0, len) (OUT = B2, or B after the bitonic fallback)
-// and `mn` holds min.  B, B2: NT*ITEMS u64 smem; fh: NT*ITEMS u32 smem.  Ends with a barrier.
+// the sorted (ok - min) values are in B[0, len) and `mn` holds min.  B: NT*ITEMS u64 smem;
+// fh: NT*ITEMS u32 smem.  Ends with a barrier.
 #ifdef IPLS_BASE_TIMING  // dev harness only: per-phase clock accumulation by thread 0
 __device__ unsigned long long g_base_phase[16];
 #define BASE_TICK(N)                                                         \
@@ -1398,7 +1401,7 @@ __device__ unsigned long long g_base_phase[16];
 #define BASE_TICK(N)
 #endif
 template <int NT, int ITEMS>
-__device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint64_t* B, uint64_t* B2,
+__device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint64_t* B,
                                        uint32_t* fh, BaseSmem& ss, uint64_t& mn_out,
                                        long long& t_prev_) {
   constexpr int NW = NT / 32;
@@ -1435,9 +1438,9 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
   if (mn == mx) {  // constant window: every key is mn
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j)
-      if (j * NT + threadIdx.x < len) B2[j * NT + threadIdx.x] = 0;
+      if (j * NT + threadIdx.x < len) B[j * NT + threadIdx.x] = 0;
     __syncthreads();
-    return B2;
+    return B;
   }
   const int bl = 64 - __clzll((long long)(mx - mn));
   const int sh = bl > 8 ? bl - 8 : 0;
@@ -1468,7 +1471,7 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
   __syncthreads();
   BASE_TICK(5);
   // exclusive scan of the NT*ITEMS fine-bin counts: thread t owns bins [ITEMS t, ITEMS t + ITEMS)
-  uint32_t mxc = 0;
+  uint32_t mxc = 0, lo, hi;  // this thread's fine bins hold B[lo, hi) after placement
   {
     uint4* f4 = reinterpret_cast<uint4*>(fh) + threadIdx.x * (ITEMS / 4);
     uint32_t sum = 0;
@@ -1479,6 +1482,8 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
       mxc = max(mxc, max(max(c.x, c.y), max(c.z, c.w)));
     }
     uint32_t run = block_exclusive_scan<NT>(sum, ss.warp, nullptr);
+    lo = run;
+    hi = run + sum;
 #pragma unroll
     for (int q = 0; q < ITEMS / 4; ++q) {
       const uint4 c = f4[q];
@@ -1506,40 +1511,46 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
     bitonic_sort_smem<NT>(B, len);
     return B;
   }
-  // fh[f] is now the end of fine bin f.  Every key counts the keys of its bin that precede
-  // it (smaller, or equal at a smaller slot) and lands at bin start + that rank.
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    if (j * NT + threadIdx.x < len) {
-      const uint32_t f = fs[j] & 0xffffu, slot = fs[j] >> 16;
-      const uint32_t beg = f ? fh[f - 1] : 0u, end = fh[f];
-      const uint64_t d = v[j];
-      uint32_t r = beg;
-      for (uint32_t q = beg; q < end; ++q) {
-        const uint64_t y = B[q];
-        r += (y < d || (y == d && q < slot)) ? 1u : 0u;
+  // B is ordered across fine bins: every thread insertion-sorts its range B[lo, hi) (only
+  // in-bin inversions move; each key moves at most its bin's load - 1 places).
+  if (lo < hi) {
+    uint64_t prev = B[lo];
+    for (uint32_t i = lo + 1; i < hi; ++i) {
+      const uint64_t x = B[i];
+      if (x < prev) {
+        uint32_t j = i;
+        uint64_t y = prev;
+        do {
+          B[j] = y;
+          --j;
+          y = (j > lo) ? B[j - 1] : 0ull;
+        } while (j > lo && y > x);
+        B[j] = x;
+      } else {
+        prev = x;
       }
-      B2[r] = d;
     }
   }
   __syncthreads();
   BASE_TICK(8);
-  return B2;
+  return B;
 }
 
 // One window of big base children (<= kBigCap keys) per CTA: 512 threads, 8 keys per thread
-// in registers, 2 CTAs per SM (80 KB smem each), so one CTA's barriers and load latency
-// overlap the other's work.
+// in registers, 3 CTAs per SM (48 KB smem each), so one CTA's barriers and load latency
+// overlap the others' work.
 
 template <bool F64, bool NANCHK>
-__global__ __launch_bounds__(kBCThreads, 2) void k_base_sort(
+#ifndef IPLS_BS_OCC
+#define IPLS_BS_OCC 3
+#endif
+__global__ __launch_bounds__(kBCThreads, IPLS_BS_OCC) void k_base_sort(
     const Window* __restrict__ wins, uint64_t* __restrict__ user, const uint64_t* __restrict__ scr,
     uint32_t* __restrict__ err) {
   constexpr int NT = kBCThreads, ITEMS = kBCItems;
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* A = reinterpret_cast<uint64_t*>(smraw);           // kBigCap: placement array
-  uint64_t* B2 = A + kBigCap;                                  // kBigCap
-  uint32_t* fh = reinterpret_cast<uint32_t*>(B2 + kBigCap);    // kBigCap
+  uint32_t* fh = reinterpret_cast<uint32_t*>(A + kBigCap);     // kBigCap
   __shared__ BaseSmem ss;
   long long t_prev_ = 0;
   const Window wv = wins[blockIdx.x];
@@ -1563,7 +1574,7 @@ __global__ __launch_bounds__(kBCThreads, 2) void k_base_sort(
     }
   }
   uint64_t mn;
-  const uint64_t* out = sort_regs_to_smem<NT, ITEMS>(v, len, A, B2, fh, ss, mn, t_prev_);
+  const uint64_t* out = sort_regs_to_smem<NT, ITEMS>(v, len, A, fh, ss, mn, t_prev_);
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     const uint32_t i = j * NT + threadIdx.x;
@@ -1622,9 +1633,7 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
   constexpr int BPL = kWBBins / 32;  // bins per lane
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   uint64_t* IN = reinterpret_cast<uint64_t*>(smraw + wp * kWBSmemPerWarp);  // 2 x kWBStride
-  uint32_t* FS = reinterpret_cast<uint32_t*>(IN + 2 * kWBStride);            // kWBCap
-  uint32_t* bins = FS + kWBCap;                                              // kWBBins + 32
-  uint64_t* T = reinterpret_cast<uint64_t*>(bins);                           // rank buffer
+  uint32_t* bins = reinterpret_cast<uint32_t*>(IN + 2 * kWBStride);          // kWBBins + 32
   uint64_t* mbar = s_mbar[wp];
   const uint32_t gw = blockIdx.x * kWBWarps + wp, gstride = gridDim.x * kWBWarps;
   // lane 0: start the bulk copy of the window described by wv into IN[b].  Descriptors are
@@ -1746,7 +1755,7 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       // lane-contiguous scan walk is conflict-free.
       for (uint32_t q = lane; q < (uint32_t)(kWBBins + 32); q += 32) bins[q] = 0u;
       __syncwarp();
-      uint32_t fr[kWBItems];  // bin, then bin | slot << 16
+      uint32_t fr[kWBItems];  // bin
 #pragma unroll
       for (int j = 0; j < kWBItems; ++j) {
         fr[j] = 0;
@@ -1761,7 +1770,8 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       }
       __syncwarp();
     WB_TICK(3);
-      uint32_t mxc = 0;
+      // Lane l owns bins [BPL l, BPL l + BPL): after the scan its keys occupy B[lo, hi).
+      uint32_t mxc = 0, lo, hi;
       {
         uint32_t* bl0 = bins + lane * BPL + ((lane * BPL) >> 5);
         uint32_t sum = 0;
@@ -1777,7 +1787,9 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
           const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
           if (lane >= o) inc += y;
         }
-        uint32_t run = inc - sum;
+        lo = inc - sum;
+        hi = inc;
+        uint32_t run = lo;
 #pragma unroll 8
         for (int q = 0; q < BPL; ++q) {
           const uint32_t c = bl0[q];
@@ -1792,9 +1804,7 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       for (int j = 0; j < kWBItems; ++j) {
         if (j * 32 + lane < len) {
           const uint32_t fb = fr[j];
-          const uint32_t slot = atomicAdd(&bins[fb + (fb >> 5)], 1u);
-          B[slot] = v[j];
-          fr[j] = fb | (slot << 16);
+          B[atomicAdd(&bins[fb + (fb >> 5)], 1u)] = v[j];
         }
       }
       __syncwarp();
@@ -1803,46 +1813,26 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
         warp_bitonic_ok<F64>(B, len, lane);
         OUT = B;
       } else {
-        // bins hold bin ends now.  Keys alone in their bin are already in place in B.  Keys
-        // of multi-key bins (a minority) are compacted into a worklist (FS); each ranks itself
-        // among its bin (smaller, or equal at a smaller slot) and is written to T (the dead
-        // bins region) at bin start + rank, then copied back to B.
-        uint32_t nwork = 0;
-#pragma unroll
-        for (int jj = 0; jj < kWBItems; ++jj) {
-          const uint32_t i = jj * 32 + lane;
-          uint32_t item = 0;
-          bool multi = false;
-          if (i < len) {
-            const uint32_t w = fr[jj];
-            const uint32_t fb = w & 0xffffu, slot = w >> 16;
-            const uint32_t beg = fb ? bins[(fb - 1) + ((fb - 1) >> 5)] : 0u;
-            const uint32_t end = bins[fb + (fb >> 5)];
-            multi = end - beg > 1;
-            item = slot | (beg << 10) | ((end - beg) << 20);
+        // B is ordered across bins; each lane insertion-sorts its own range B[lo, hi) (every
+        // key moves at most (its bin's load - 1) places; most keys do not move at all).
+        // Keys compare as (bits ^ flip) (one-signed window); equal keys are equal bits.
+        if (lo < hi) {
+          uint64_t prev = B[lo] ^ flip;
+          for (uint32_t i = lo + 1; i < hi; ++i) {
+            const uint64_t x = B[i] ^ flip;
+            if (x < prev) {
+              uint32_t j = i;
+              uint64_t y = prev;
+              do {
+                B[j] = y ^ flip;
+                --j;
+                y = (j > lo) ? (B[j - 1] ^ flip) : 0ull;
+              } while (j > lo && y > x);
+              B[j] = x ^ flip;
+            } else {
+              prev = x;
+            }
           }
-          const uint32_t mask = __ballot_sync(0xffffffffu, multi);
-          if (multi) FS[nwork + __popc(mask & ((1u << lane) - 1u))] = item;
-          nwork += __popc(mask);
-        }
-        __syncwarp();
-    WB_TICK(6);
-        for (uint32_t j = lane; j < nwork; j += 32) {
-          const uint32_t item = FS[j];
-          const uint32_t slot = item & 1023u, beg = (item >> 10) & 1023u, n = item >> 20;
-          const uint64_t x = B[slot] ^ flip;
-          uint32_t r = beg;
-          for (uint32_t p = beg; p < beg + n; ++p) {
-            const uint64_t y = B[p] ^ flip;
-            r += (y < x || (y == x && p < slot)) ? 1u : 0u;
-          }
-          T[r] = x ^ flip;
-        }
-        __syncwarp();
-    WB_TICK(7);
-        for (uint32_t j = lane; j < nwork; j += 32) {
-          const uint32_t slot = FS[j] & 1023u;
-          B[slot] = T[slot];
         }
         OUT = B;
       }
