@@ -1818,8 +1818,10 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
         // Keys compare as (bits ^ flip) (one-signed window); equal keys are equal bits.
         if (lo < hi) {
           uint64_t prev = B[lo] ^ flip;
+          uint64_t nx = B[lo + 1];  // B[i + 1] is never written while key i is inserted
           for (uint32_t i = lo + 1; i < hi; ++i) {
-            const uint64_t x = B[i] ^ flip;
+            const uint64_t x = nx ^ flip;
+            nx = B[i + 1];  // (may read one slot past the window: within IN[b], unused)
             if (x < prev) {
               uint32_t j = i;
               uint64_t y = prev;
@@ -1838,7 +1840,11 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       }
     }
     __syncwarp();
-    for (uint32_t i = lane; i < len; i += 32) __stcs(dst + i, OUT[i]);
+#pragma unroll
+    for (int j = 0; j < kWBItems; ++j) v[j] = OUT[j * 32 + lane];
+#pragma unroll
+    for (int j = 0; j < kWBItems; ++j)
+      if (j * 32 + lane < len) __stcs(dst + j * 32 + lane, v[j]);
     WB_TICK(8);
     fence_proxy_async_smem();  // generic accesses to IN[b] before the bulk copy that reuses it
     __syncwarp();
