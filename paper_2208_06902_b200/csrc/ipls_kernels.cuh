@@ -1737,6 +1737,7 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       range = (double)(umx - umn);
     }
     const uint64_t* OUT = K;  // constant (u64) windows are already sorted
+    uint64_t oflip = 0;       // OUT holds bits ^ oflip
     WB_TICK(2);
     if (!F64 && umn == umx) {
       // nothing to sort
@@ -1804,44 +1805,51 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       for (int j = 0; j < kWBItems; ++j) {
         if (j * 32 + lane < len) {
           const uint32_t fb = fr[j];
-          B[atomicAdd(&bins[fb + (fb >> 5)], 1u)] = v[j];
+          B[atomicAdd(&bins[fb + (fb >> 5)], 1u)] = v[j] ^ flip;  // u64 key order
         }
       }
       __syncwarp();
     WB_TICK(5);
       if (overflow) {
+        for (uint32_t i = lane; i < len; i += 32) B[i] ^= flip;
+        __syncwarp();
         warp_bitonic_ok<F64>(B, len, lane);
         OUT = B;
       } else {
-        // B is ordered across bins; each lane insertion-sorts its own range B[lo, hi) (every
-        // key moves at most (its bin's load - 1) places; most keys do not move at all).
-        // Keys compare as (bits ^ flip) (one-signed window); equal keys are equal bits.
+        // B is ordered across bins; each lane insertion-sorts its own range B[lo, hi): every
+        // key moves at most (its bin's load - 1) places.  The last two keys of the sorted
+        // prefix stay in registers (pp <= prev), so a key that moves by at most one place
+        // (nearly all of them) costs no branch; only a key below both walks the prefix.
         if (lo < hi) {
-          uint64_t prev = B[lo] ^ flip;
-          uint64_t nx = B[lo + 1];  // B[i + 1] is never written while key i is inserted
-          for (uint32_t i = lo + 1; i < hi; ++i) {
-            const uint64_t x = nx ^ flip;
-            nx = B[i + 1];  // (may read one slot past the window: within IN[b], unused)
+          uint64_t* q = B + lo;  // q[1] is the key being inserted
+          uint64_t prev = q[0], pp = 0ull, nx = q[1];
+          for (uint32_t i = lo + 1; i < hi; ++i, ++q) {
+            const uint64_t x = nx;
+            nx = q[2];  // never written while x is inserted (may read 1 slot past the window)
             if (x < prev) {
-              uint32_t j = i;
-              uint64_t y = prev;
-              do {
-                B[j] = y ^ flip;
-                --j;
-                y = (j > lo) ? (B[j - 1] ^ flip) : 0ull;
-              } while (j > lo && y > x);
-              B[j] = x ^ flip;
+              q[1] = prev;
+              if (x >= pp) {
+                q[0] = x;
+                pp = x;
+              } else {  // rare: x belongs below pp
+                q[0] = pp;
+                uint64_t* r = q - 1;
+                while (r > B + lo && r[-1] > x) { r[0] = r[-1]; --r; }
+                r[0] = x;
+              }
             } else {
+              pp = prev;
               prev = x;
             }
           }
         }
+        oflip = flip;
         OUT = B;
       }
     }
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < kWBItems; ++j) v[j] = OUT[j * 32 + lane];
+    for (int j = 0; j < kWBItems; ++j) v[j] = OUT[j * 32 + lane] ^ oflip;
 #pragma unroll
     for (int j = 0; j < kWBItems; ++j)
       if (j * 32 + lane < len) __stcs(dst + j * 32 + lane, v[j]);
