@@ -1513,20 +1513,27 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
   }
   // B is ordered across fine bins: every thread insertion-sorts its range B[lo, hi) (only
   // in-bin inversions move; each key moves at most its bin's load - 1 places).
+  // The last two keys of the sorted prefix stay in registers (pp <= prev): a key that moves by
+  // at most one place costs no branch; only a key below both walks the prefix.
   if (lo < hi) {
-    uint64_t prev = B[lo];
-    for (uint32_t i = lo + 1; i < hi; ++i) {
-      const uint64_t x = B[i];
+    uint64_t* q = B + lo;  // q[1] is the key being inserted
+    uint64_t prev = q[0], pp = 0ull, nx = (lo + 1 < hi) ? q[1] : 0ull;
+    for (uint32_t i = lo + 1; i < hi; ++i, ++q) {
+      const uint64_t x = nx;
+      nx = (i + 1 < hi) ? q[2] : 0ull;  // never written while x is inserted
       if (x < prev) {
-        uint32_t j = i;
-        uint64_t y = prev;
-        do {
-          B[j] = y;
-          --j;
-          y = (j > lo) ? B[j - 1] : 0ull;
-        } while (j > lo && y > x);
-        B[j] = x;
+        q[1] = prev;
+        if (x >= pp) {
+          q[0] = x;
+          pp = x;
+        } else {  // rare: x belongs below pp
+          q[0] = pp;
+          uint64_t* r = q - 1;
+          while (r > B + lo && r[-1] > x) { r[0] = r[-1]; --r; }
+          r[0] = x;
+        }
       } else {
+        pp = prev;
         prev = x;
       }
     }
