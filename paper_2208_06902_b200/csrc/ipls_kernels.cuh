@@ -1830,24 +1830,23 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
         if (lo < hi) {
           uint64_t* q = B + lo;  // q[1] is the key being inserted
           uint64_t prev = q[0], pp = 0ull, nx = q[1];
+#pragma unroll 2
           for (uint32_t i = lo + 1; i < hi; ++i, ++q) {
             const uint64_t x = nx;
             nx = q[2];  // never written while x is inserted (may read 1 slot past the window)
-            if (x < prev) {
+            const bool lt = x < prev;
+            const uint64_t m = max(pp, x);
+            if (lt) {
               q[1] = prev;
-              if (x >= pp) {
-                q[0] = x;
-                pp = x;
-              } else {  // rare: x belongs below pp
-                q[0] = pp;
-                uint64_t* r = q - 1;
-                while (r > B + lo && r[-1] > x) { r[0] = r[-1]; --r; }
-                r[0] = x;
-              }
-            } else {
-              pp = prev;
-              prev = x;
+              q[0] = m;
             }
+            if (lt && x < pp) {  // rare: x belongs below pp (q[0] = pp already)
+              uint64_t* r = q - 1;
+              while (r > B + lo && r[-1] > x) { r[0] = r[-1]; --r; }
+              r[0] = x;
+            }
+            pp = lt ? m : prev;
+            prev = lt ? prev : x;
           }
         }
         oflip = flip;
