@@ -1246,10 +1246,17 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
     const uint32_t i = wp * (kURounds * 32) + r * 32 + lane;
     key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
   }
+#ifdef IPLS_SCATTER_TIMING
+  long long t_prev_ = clock64();
+#endif
   for (uint32_t t0 = 0; t0 < ch.len; t0 += kUTile) {
     const uint32_t tl = min((uint32_t)kUTile, ch.len - t0);
     for (uint32_t b = threadIdx.x; b < k; b += NT) cnt[b] = 0u;
     __syncthreads();
+#ifdef IPLS_SCATTER_TIMING
+    if (threadIdx.x == 0) atomicAdd(&g_sc_phase[15], 1ull);
+#endif
+    SC_TICK(11);
     uint32_t bk[kURounds / 2];  // two buckets per word; 0xffff = no key
 #pragma unroll
     for (int r = 0; r < kURounds; ++r) {
@@ -1263,6 +1270,7 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
       else bk[r >> 1] = bb;
     }
     __syncthreads();
+    SC_TICK(12);
     {
       uint32_t cc[kSBpt], sum = 0;
 #pragma unroll
@@ -1285,6 +1293,7 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
       }
     }
     __syncthreads();
+    SC_TICK(13);
 #pragma unroll
     for (int r = 0; r < kURounds; ++r) {
       const uint32_t bb = (bk[r >> 1] >> (16 * (r & 1))) & 0xffffu;
@@ -1300,9 +1309,11 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
       key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
     }
     __syncthreads();
+    SC_TICK(14);
     for (uint32_t q = threadIdx.x; q < tl; q += NT)
       st_evict_last(reinterpret_cast<uint64_t*>(adj[sbk[q]]) + q, stage[q]);
     __syncthreads();
+    SC_TICK(7);
   }
 }
 

@@ -29,5 +29,8 @@ lib.ipls_debug_scatter_phases(ph, 1)
 tr = ipls.sort_trace(src.clone(), k=cfg.k, base_case=cfg.base_case, key_type=kt) if False else None
 tiles = sum((int(n) + 8191) // 8192 for n in [a.size]) * 2  # approx: 2 levels over all keys
 print("scatter cycles per tile (thread 0):", " ".join(f"{i}:{ph[i] / tiles:.0f}" for i in range(7)))
+nt = max(ph[15], 1)
+print(f"unstable scatter: {ph[15]} tiles; cycles per tile (thread 0): zero {ph[11]/nt:.0f} count {ph[12]/nt:.0f} "
+      f"scan {ph[13]/nt:.0f} place {ph[14]/nt:.0f} writeout {ph[7]/nt:.0f}")
 print("fit cycle sums over all CTAs of the last sort (x1e6): gather", ph[8] / 1e6, "sort", ph[9] / 1e6,
       "fmcd", ph[10] / 1e6)
