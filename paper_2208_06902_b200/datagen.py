@@ -128,6 +128,33 @@ def fuzz_array(rng: np.random.Generator, n: int, kind: str) -> np.ndarray:
     raise KeyError(kind)
 
 
+def stress_array(rng: np.random.Generator, n: int, kind: str) -> np.ndarray:
+    """Inputs that load the base case's bins: tight clusters of near-equal keys (several keys
+    per interpolation bin, in every order), one sign per window or windows through zero,
+    u64 keys that collide in binary64.  Shuffled.  No method arithmetic."""
+    if kind in ("clusters3", "clusters40", "neg_clusters"):
+        c = 3 if kind != "clusters40" else 40
+        m = (n + c - 1) // c
+        centers = rng.random(m) * 1e3
+        if kind == "neg_clusters":
+            centers = -1.0 - centers
+        v = np.repeat(centers, c)[:n] + rng.integers(0, 4, n) * 1e-9
+    elif kind == "zero_straddle":
+        v = rng.normal(0.0, 1e-300, n)
+        v[rng.random(n) < 0.01] = 0.0
+        v[rng.random(n) < 0.01] = -0.0
+    elif kind == "u64_clusters":
+        m = (n + 2) // 3
+        centers = rng.integers(2**60, 2**63, m, dtype=np.uint64)
+        v = np.repeat(centers, 3)[:n] + rng.integers(0, 8, n, dtype=np.uint64)
+    else:
+        raise KeyError(kind)
+    rng.shuffle(v)
+    return v
+
+
+STRESS_KINDS = ["clusters3", "clusters40", "neg_clusters", "zero_straddle", "u64_clusters"]
+
 FUZZ_KINDS = ["uniform", "normal", "lognormal", "all_equal", "two_values", "signed_zeros",
               "zeros_mixed", "denormals", "infs", "sorted", "reverse", "few_distinct",
               "root_dups_u64", "u64_big", "u64_above_2_53", "mixture", "exponential"]

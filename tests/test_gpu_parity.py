@@ -186,6 +186,21 @@ def test_sort_parity_fuzz(ipls, kind, size):
         assert np.array_equal(g, w), f"layout after level {lv} differs"
 
 
+@pytest.mark.parametrize("kind", datagen.STRESS_KINDS)
+@pytest.mark.parametrize("n,k", [(300_000, 1024), (1_000_003, 256), (2_000_000, 1024)])
+def test_base_case_stress_parity(ipls, kind, n, k):
+    """Clustered keys put several keys (in every order, up to > kFineOverflow) into one
+    interpolation bin of the base case: warp windows (k=1024: children ~100-300 keys) and
+    CTA windows (k=256 at 1e6: children ~4k keys); negative, zero-straddling and u64 windows."""
+    rng = np.random.default_rng(n + k + len(kind))
+    a = datagen.stress_array(rng, n, kind)
+    want = a.copy()
+    oracle.sort(want, k=k, base_case=4096)
+    t = dev(a)
+    ipls.sort(t, k=k, base_case=4096, key_type=kt_of(a))
+    assert host(t, a.dtype).tobytes() == want.tobytes()
+
+
 def test_worked_example_sort(ipls, golden):
     x = np.array([float(v) for v in golden("worked_example.txt")["input"][0]])
     t = dev(x)
