@@ -165,6 +165,30 @@ __host__ __device__ __forceinline__ uint32_t sample_size(uint64_t m, uint32_t k)
   return (uint32_t)S;
 }
 
+// Stratum bounds lo_j = floor(j m / S), hi_j = floor((j+1) m / S) (R2) for j = j0, j0 + step,
+// j0 + 2 step, ... with three divisions per thread instead of two 64-bit divisions per
+// sample: exact recurrences on (quotient, remainder) of j m / S.
+struct StrataWalk {
+  uint64_t q, r;    // floor(j m / S), j m mod S
+  uint64_t sq, sr;  // floor(step m / S), step m mod S
+  uint64_t mq, mr;  // floor(m / S), m mod S: lo_{j+1} = lo_j + mq + (r + mr >= S)
+  uint64_t S;
+  __device__ __forceinline__ StrataWalk(uint32_t j0, uint32_t step, uint64_t m, uint32_t S_)
+      : S(S_) {
+    const uint64_t a = (uint64_t)j0 * m, b = (uint64_t)step * m;
+    q = a / S; r = a - q * S;
+    sq = b / S; sr = b - sq * S;
+    mq = m / S; mr = m - mq * S;
+  }
+  __device__ __forceinline__ uint64_t lo() const { return q; }
+  __device__ __forceinline__ uint64_t hi() const { return q + mq + (r + mr >= S ? 1u : 0u); }
+  __device__ __forceinline__ void next() {
+    q += sq;
+    r += sr;
+    if (r >= S) { r -= S; ++q; }
+  }
+};
+
 // ---- block-wide exclusive scan of one uint32 per thread (blockDim multiple of 32) ----
 template <int NT>
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t* s_warp,

@@ -246,10 +246,9 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     __syncthreads();
   } else {
     const uint64_t t = sm64(sm64(sm64(seed) ^ (uint64_t)level) ^ sg.begin);
-    const uint64_t m = sg.m;
-    for (uint32_t j = threadIdx.x; j < S; j += kFitThreads) {
-      uint64_t lo = ((uint64_t)j * m) / S;
-      uint64_t hi = ((uint64_t)(j + 1) * m) / S;
+    StrataWalk sw(threadIdx.x, kFitThreads, sg.m, S);
+    for (uint32_t j = threadIdx.x; j < S; j += kFitThreads, sw.next()) {
+      const uint64_t lo = sw.lo(), hi = sw.hi();
       uint64_t h = sm64(t ^ (uint64_t)j);
       uint64_t idx = sg.begin + lo + __umul64hi(h, hi - lo);
       a[j] = ok_of<F64>(__ldg(src + idx));
@@ -347,7 +346,7 @@ __global__ __launch_bounds__(kFSThreads, 3) void k_fit_small(
   }
   // ---- stratified sample (R2, R18), as ordering keys in registers ----
   const uint64_t t = sm64(sm64(sm64(seed) ^ (uint64_t)level) ^ sg.begin);
-  const uint64_t m = sg.m;
+  StrataWalk sw(threadIdx.x, NT, sg.m, S);
   uint64_t v[IT];
   uint64_t mn = ~0ull, mx = 0ull;
 #pragma unroll
@@ -355,13 +354,13 @@ __global__ __launch_bounds__(kFSThreads, 3) void k_fit_small(
     const uint32_t j = r * NT + threadIdx.x;
     v[r] = 0;
     if (j < S) {
-      const uint64_t lo = ((uint64_t)j * m) / S;
-      const uint64_t hi = ((uint64_t)(j + 1) * m) / S;
+      const uint64_t lo = sw.lo(), hi = sw.hi();
       const uint64_t idx = sg.begin + lo + __umul64hi(sm64(t ^ (uint64_t)j), hi - lo);
       v[r] = ok_of<F64>(__ldg(src + idx));
       mn = min(mn, v[r]);
       mx = max(mx, v[r]);
     }
+    sw.next();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
