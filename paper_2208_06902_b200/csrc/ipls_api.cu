@@ -291,8 +291,10 @@ void set_attrs() {
   if (done) return;
   ck(cudaFuncSetAttribute(k_gather_fit<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)fit_smem(kFitMaxS)));
-  ck(cudaFuncSetAttribute(k_fit_small<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)kFSSmem));
+  ck(cudaFuncSetAttribute(k_fit_small<F64, kFSThreads, kFSItems>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSSmem));
+  ck(cudaFuncSetAttribute(k_fit_small<F64, kFLThreads, kFLItems>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFLSmem));
   ck(cudaFuncSetAttribute(k_base_sort<F64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)base_smem()));
   ck(cudaFuncSetAttribute(k_base_sort<F64, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -398,8 +400,12 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
       IPLS_PROF("gather_fit", 0);
       const uint32_t cap = fit_cap(max_S);
       uint32_t* redo = at<uint32_t>(meta, ML.seg_term);  // scratch until K2 writes seg_term
-      k_fit_small<F64><<<nseg, kFSThreads, kFSSmem, st>>>(src, segs, seed, level, k,
-                                                          trace ? samples : nullptr, models, redo);
+      if (max_S <= (uint32_t)kFSMax)
+        k_fit_small<F64, kFSThreads, kFSItems><<<nseg, kFSThreads, kFSSmem, st>>>(
+            src, segs, seed, level, k, trace ? samples : nullptr, models, redo);
+      else
+        k_fit_small<F64, kFLThreads, kFLItems><<<nseg, kFLThreads, kFLSmem, st>>>(
+            src, segs, seed, level, k, trace ? samples : nullptr, models, redo);
       ck_launch();
       k_gather_fit<F64><<<nseg, kFitThreads, fit_smem(cap), st>>>(
           src, segs, seed, level, k, cap, trace ? samples : nullptr, models, nullptr, redo);
@@ -794,9 +800,9 @@ uint64_t ipls_kernel_launch_count(void) { return g_launches.load(); }
 #ifdef IPLS_SCATTER_TIMING
 // dev builds only (tools/phase_scatter.py): per-phase cycle sums of thread 0 of every CTA
 void ipls_debug_scatter_phases(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, g_sc_phase, sizeof(unsigned long long) * 16);
+  cudaMemcpyFromSymbol(out, g_sc_phase, sizeof(unsigned long long) * 32);
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[32] = {0};
     cudaMemcpyToSymbol(g_sc_phase, z, sizeof(z));
   }
 }

@@ -18,7 +18,7 @@
 namespace ipls {
 
 #ifdef IPLS_SCATTER_TIMING  // dev builds only (tools/phase_scatter.py)
-__device__ unsigned long long g_sc_phase[16];
+__device__ unsigned long long g_sc_phase[32];
 #define FIT_TICK(N) do { if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_sc_phase[N], (unsigned long long)(t_ - ft_prev_)); ft_prev_ = t_; } } while (0)
 #else
 #define FIT_TICK(N)
@@ -61,6 +61,8 @@ constexpr uint32_t kFineOverflow = 32;          // fine-bin load that triggers t
 struct SortSmem {
   uint32_t ccnt[256];
   uint32_t coff[256];
+  uint32_t ccnt2[256];  // k_fit_small: coarse counts in the other key space
+  uint32_t cmax[2];
   uint64_t red[64];
   uint32_t warp[40];
 };
@@ -247,11 +249,22 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
   } else {
     const uint64_t t = sm64(sm64(sm64(seed) ^ (uint64_t)level) ^ sg.begin);
     StrataWalk sw(threadIdx.x, kFitThreads, sg.m, S);
-    for (uint32_t j = threadIdx.x; j < S; j += kFitThreads, sw.next()) {
-      const uint64_t lo = sw.lo(), hi = sw.hi();
-      uint64_t h = sm64(t ^ (uint64_t)j);
-      uint64_t idx = sg.begin + lo + __umul64hi(h, hi - lo);
-      a[j] = ok_of<F64>(__ldg(src + idx));
+    // batches of 8 loads in flight per thread (S <= cap <= 8 kFitThreads)
+    for (uint32_t j0 = threadIdx.x; j0 < S; j0 += 8 * kFitThreads) {
+      uint64_t x[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const uint32_t j = j0 + r * kFitThreads;
+        const uint64_t lo = sw.lo(), hi = sw.hi();
+        const uint64_t idx = sg.begin + lo + __umul64hi(sm64(t ^ (uint64_t)j), hi - lo);
+        x[r] = __ldg(src + (j < S ? idx : sg.begin));
+        sw.next();
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const uint32_t j = j0 + r * kFitThreads;
+        if (j < S) a[j] = ok_of<F64>(x[r]);
+      }
     }
     __syncthreads();
     FIT_TICK(8);
@@ -325,48 +338,68 @@ constexpr int kFSThreads = 256;
 constexpr int kFSItems = 20;                     // samples per thread
 constexpr int kFSMax = kFSThreads * kFSItems;    // 5120 (S(m) for m <= 2^25 at k = 1024)
 constexpr size_t kFSSmem = (size_t)kFSMax * 12;
+// Large-sample variant (one CTA of 1024 threads, 8 samples each: every S(m) <= 7k - 1 < 8192),
+// used for the levels whose largest sample exceeds kFSMax (level 0 at >= 2^25 keys).
+constexpr int kFLThreads = 1024;
+constexpr int kFLItems = 8;
+constexpr int kFLMax = kFLThreads * kFLItems;    // 8192
+constexpr size_t kFLSmem = (size_t)kFLMax * 12;
 
-template <bool F64>
-__global__ __launch_bounds__(kFSThreads, 3) void k_fit_small(
+template <bool F64, int NT, int IT>
+__global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
     const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
     uint32_t level, uint32_t k, uint64_t* __restrict__ samples_out, ModelDev* __restrict__ models,
     uint32_t* __restrict__ redo) {
-  constexpr int NT = kFSThreads, NW = NT / 32, IT = kFSItems;
+  constexpr int NW = NT / 32, SMAX = NT * IT;
+  static_assert(NT >= 256 && IT % 4 == 0, "256 coarse bins, uint4 fine-bin scan");
   extern __shared__ __align__(128) unsigned char smraw[];
-  uint64_t* B = reinterpret_cast<uint64_t*>(smraw);      // kFSMax
-  uint32_t* fh = reinterpret_cast<uint32_t*>(B + kFSMax);  // kFSMax
+  uint64_t* B = reinterpret_cast<uint64_t*>(smraw);      // SMAX
+  uint32_t* fh = reinterpret_cast<uint32_t*>(B + SMAX);  // SMAX
   __shared__ SortSmem ss;
   __shared__ uint64_t s_pivot;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const SegDesc sg = segs[blockIdx.x];
   const uint32_t S = sg.S;
-  if (S > (uint32_t)kFSMax) {
+  if (S > (uint32_t)SMAX) {
     if (threadIdx.x == 0) redo[blockIdx.x] = 1u;
     return;
   }
   // ---- stratified sample (R2, R18), as ordering keys in registers ----
+#ifdef IPLS_SCATTER_TIMING
+  long long ft_prev_ = clock64();
+#define FITL_TICK(N) do { if (NT == 1024) FIT_TICK(N); else if ((N) < 22) FIT_TICK((N) + 3); } while (0)
+#else
+#define FITL_TICK(N)
+#endif
   const uint64_t t = sm64(sm64(sm64(seed) ^ (uint64_t)level) ^ sg.begin);
   StrataWalk sw(threadIdx.x, NT, sg.m, S);
   uint64_t v[IT];
   uint64_t mn = ~0ull, mx = 0ull;
+  // all IT loads are issued before any is used (one DRAM latency per thread, not IT)
 #pragma unroll
   for (int r = 0; r < IT; ++r) {
     const uint32_t j = r * NT + threadIdx.x;
-    v[r] = 0;
-    if (j < S) {
-      const uint64_t lo = sw.lo(), hi = sw.hi();
-      const uint64_t idx = sg.begin + lo + __umul64hi(sm64(t ^ (uint64_t)j), hi - lo);
-      v[r] = ok_of<F64>(__ldg(src + idx));
+    const uint64_t lo = sw.lo(), hi = sw.hi();
+    const uint64_t idx = sg.begin + lo + __umul64hi(sm64(t ^ (uint64_t)j), hi - lo);
+    v[r] = __ldg(src + (j < S ? idx : sg.begin));
+    sw.next();
+  }
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    if (r * NT + threadIdx.x < S) {
+      v[r] = ok_of<F64>(v[r]);
       mn = min(mn, v[r]);
       mx = max(mx, v[r]);
+    } else {
+      v[r] = 0;
     }
-    sw.next();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
+  FITL_TICK(16);
   if (lane == 0) { ss.red[wp] = mn; ss.red[32 + wp] = mx; }
   for (uint32_t c = threadIdx.x; c < 256; c += NT) ss.ccnt[c] = 0u;
   {
@@ -375,6 +408,7 @@ __global__ __launch_bounds__(kFSThreads, 3) void k_fit_small(
     for (int q = 0; q < IT / 4; ++q) f4[q] = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
+    FITL_TICK(22);
   mn = ss.red[0]; mx = ss.red[32];
 #pragma unroll
   for (int w = 1; w < NW; ++w) { mn = min(mn, ss.red[w]); mx = max(mx, ss.red[32 + w]); }
@@ -388,26 +422,74 @@ __global__ __launch_bounds__(kFSThreads, 3) void k_fit_small(
   } else {
     const int bl = 64 - __clzll((long long)(mx - mn));
     const int sh = bl > 8 ? bl - 8 : 0;
+    // f64: bins in key-value space (linear in the key) whenever the range allows it.
+    // Ordering-key space is linear only inside a binade, so a sample spanning many binades
+    // (a Normal around 0 at level 0) piles into a few coarse bins and long insertion runs.
+    // Heavy-tailed samples (a LogNormal) are the opposite case, so both coarse histograms
+    // are built and the space with the smaller largest coarse bin is used.
+    bool lin = false;
+    double vmn = 0.0, vsc = 0.0;
+    if constexpr (F64) {
+      vmn = __longlong_as_double((long long)bits_of_ok<true>(mn));
+      const double rg = __longlong_as_double((long long)bits_of_ok<true>(mx)) - vmn;
+      vsc = 256.0 / rg;
+      lin = rg > 0.0 && isfinite(rg) && isfinite(vsc);
+    }
+    auto vpos = [&](uint64_t o) -> double {  // (x - min) * 256 / range, monotone in x
+      return __dmul_rn(__dsub_rn(__longlong_as_double((long long)bits_of_ok<true>(o)), vmn), vsc);
+    };
+    if (F64 && lin) {
+      for (uint32_t c = threadIdx.x; c < 256; c += NT) ss.ccnt2[c] = 0u;
+      if (threadIdx.x < 2) ss.cmax[threadIdx.x] = 0u;
+      __syncthreads();
 #pragma unroll
-    for (int r = 0; r < IT; ++r)
-      if (r * NT + threadIdx.x < S) atomicAdd(&ss.ccnt[(uint32_t)((v[r] - mn) >> sh)], 1u);
+      for (int r = 0; r < IT; ++r)
+        if (r * NT + threadIdx.x < S) {
+          atomicAdd(&ss.ccnt[(uint32_t)((v[r] - mn) >> sh)], 1u);
+          atomicAdd(&ss.ccnt2[min(__double2uint_rz(vpos(v[r])), 255u)], 1u);
+        }
+      __syncthreads();
+      if (threadIdx.x < 256) {
+        atomicMax(&ss.cmax[0], ss.ccnt[threadIdx.x]);
+        atomicMax(&ss.cmax[1], ss.ccnt2[threadIdx.x]);
+      }
+      __syncthreads();
+      lin = ss.cmax[1] < ss.cmax[0];
+      if (lin && threadIdx.x < 256) ss.ccnt[threadIdx.x] = ss.ccnt2[threadIdx.x];
+    } else {
+#pragma unroll
+      for (int r = 0; r < IT; ++r)
+        if (r * NT + threadIdx.x < S) atomicAdd(&ss.ccnt[(uint32_t)((v[r] - mn) >> sh)], 1u);
+    }
+    const bool exact = !lin && sh == 0;  // every coarse bin is one value: counting is exact
+    auto fine_of = [&](uint64_t o) -> uint32_t {
+      if (F64 && lin) {
+        const double y = vpos(o);
+        const uint32_t c = min(__double2uint_rz(y), 255u), n = ss.ccnt[c];
+        return ss.coff[c] + min(__double2uint_rz(__dmul_rn(__dsub_rn(y, (double)c), (double)n)), n - 1);
+      }
+      return fine_bin(o, mn, sh, ss.coff, ss.ccnt);
+    };
     __syncthreads();
+    FITL_TICK(23);
     {
-      const uint32_t cc = ss.ccnt[threadIdx.x];  // NT == 256 coarse bins
+      const uint32_t cc = threadIdx.x < 256 ? ss.ccnt[threadIdx.x] : 0u;  // 256 coarse bins
       const uint32_t ex = block_exclusive_scan<NT>(cc, ss.warp, nullptr);
-      ss.coff[threadIdx.x] = ex;
+      if (threadIdx.x < 256) ss.coff[threadIdx.x] = ex;
     }
     __syncthreads();
+    FITL_TICK(24);
     uint32_t f[IT];
 #pragma unroll
     for (int r = 0; r < IT; ++r) {
       f[r] = 0;
       if (r * NT + threadIdx.x < S) {
-        f[r] = fine_bin(v[r], mn, sh, ss.coff, ss.ccnt);
+        f[r] = fine_of(v[r]);
         atomicAdd(&fh[f[r]], 1u);
       }
     }
     __syncthreads();
+    FITL_TICK(25);
     uint32_t mxc = 0;
     {
       uint4* f4 = reinterpret_cast<uint4*>(fh) + threadIdx.x * (IT / 4);
@@ -430,8 +512,7 @@ __global__ __launch_bounds__(kFSThreads, 3) void k_fit_small(
         f4[q] = o;
       }
     }
-    // sh == 0: every coarse bin is one value, the counting pass is exact
-    if (__syncthreads_or(sh > 0 && mxc > kFineOverflow)) {
+    if (__syncthreads_or(!exact && mxc > kFineOverflow)) {
       if (threadIdx.x == 0) redo[blockIdx.x] = 1u;  // the 1024-thread kernel sorts it
       return;
     }
@@ -439,7 +520,8 @@ __global__ __launch_bounds__(kFSThreads, 3) void k_fit_small(
     for (int r = 0; r < IT; ++r)
       if (r * NT + threadIdx.x < S) B[atomicAdd(&fh[f[r]], 1u)] = v[r];
     __syncthreads();
-    if (sh > 0) {
+    FITL_TICK(26);
+    if (!exact) {
       const uint32_t f0 = threadIdx.x * IT;
       const uint32_t beg = f0 ? fh[f0 - 1] : 0u, end = fh[f0 + IT - 1];
       for (uint32_t i = beg + 1; i < end; ++i) {
@@ -453,6 +535,7 @@ __global__ __launch_bounds__(kFSThreads, 3) void k_fit_small(
     }
   }
   __syncthreads();
+  FITL_TICK(17);
   if (threadIdx.x == 0) redo[blockIdx.x] = 0u;
   if (samples_out)
     for (uint32_t j = threadIdx.x; j < S; j += NT) samples_out[sg.sample_off + j] = B[j];
@@ -509,6 +592,7 @@ __global__ __launch_bounds__(kFSThreads, 3) void k_fit_small(
     md.kind = kModelEq3; md.A = 0.0; md.B = 0.0; md.D = 0; md.capped = 0;
     md.pivot_ok = s_pivot; md.k_eff = 3;
   }
+  FITL_TICK(18);
   if (threadIdx.x == 0) models[blockIdx.x] = md;
 }
 
