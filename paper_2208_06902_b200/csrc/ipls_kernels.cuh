@@ -367,7 +367,7 @@ __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
   // ---- stratified sample (R2, R18), as ordering keys in registers ----
 #ifdef IPLS_SCATTER_TIMING
   long long ft_prev_ = clock64();
-#define FITL_TICK(N) do { if (NT == 1024) FIT_TICK(N); else if ((N) < 22) FIT_TICK((N) + 3); } while (0)
+#define FITL_TICK(N) do { if (NT == 1024) { if ((N) < 22) FIT_TICK(N); } else FIT_TICK((N) < 22 ? (N) + 3 : (N)); } while (0)
 #else
 #define FITL_TICK(N)
 #endif

@@ -33,7 +33,7 @@ nt = max(ph[15], 1)
 print(f"unstable scatter: {ph[15]} tiles; cycles per tile (thread 0): zero {ph[11]/nt:.0f} count {ph[12]/nt:.0f} "
       f"scan {ph[13]/nt:.0f} place {ph[14]/nt:.0f} writeout {ph[7]/nt:.0f}")
 print(f"large-sample fit (1 CTA, cycles): gather {ph[16]} sort {ph[17]} fmcd {ph[18]}")
-print("large-sample fit sort sub-phases (cycles):", [ph[i] for i in range(22, 27)])
+print("small-sample fit sort sub-phases (cycles summed):", [ph[i] for i in range(22, 27)])
 print(f"small-sample fit (cycles summed over CTAs): gather {ph[19]} sort {ph[20]} fmcd {ph[21]}")
 print("fit cycle sums over all CTAs of the last sort (x1e6): gather", ph[8] / 1e6, "sort", ph[9] / 1e6,
       "fmcd", ph[10] / 1e6)
