@@ -1694,10 +1694,10 @@ __global__ __launch_bounds__(kBCThreads, IPLS_BS_OCC) void k_base_sort(
 // Sort = interpolation sort on the raw keys.  Bin of a key = trunc((x - min) * nb / (max -
 // min)) evaluated in binary64 (f64 keys directly, u64 keys through the exact difference
 // x - min converted to double): every step is monotone, so bins are ordered.  Counting pass
-// into smem, placement; keys alone in their bin are then in place, and the keys of multi-key
-// bins (a worklist) count the keys of their bin that precede them (ties by slot) and land at
-// bin start + that count.  Inside a window that does not reach zero all keys have one sign,
-// so raw bits ^ (negative ? 0x7ff..f : 0) compared as u64 is the key order.  Windows that
+// into smem, placement; the window is then ordered across bins and every lane insertion-sorts
+// the contiguous range of its own bins.  Inside a window that does not reach zero all keys
+// have one sign, so raw bits ^ (negative ? 0x7ff..f : 0) compared as u64 is the key order
+// (applied at placement, undone at the write-out).  Windows that
 // reach zero (they may mix -0.0 and +0.0), whose range is not finite (infinities, overflow)
 // or whose bins overflow (> kFineOverflow keys: extreme skew) take an exact warp bitonic sort
 // on ordering keys.
