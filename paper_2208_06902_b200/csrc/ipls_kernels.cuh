@@ -1911,7 +1911,29 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       }
       __syncwarp();
     WB_TICK(5);
+      // bin f occupies B[bin_beg(f), bins[f + f / 32]) now (bins hold bin ends)
+      auto bin_beg = [&](uint32_t f) -> uint32_t { return f ? bins[(f - 1) + ((f - 1) >> 5)] : 0u; };
+      bool mixed = false;  // an overflowing bin holds different keys (not just duplicates)
+      uint32_t big = 0;    // this lane's bins above kFineOverflow keys
       if (overflow) {
+        if (mxc > kFineOverflow) {
+          uint32_t e0 = lo;
+          for (int q = 0; q < BPL; ++q) {
+            const uint32_t f = lane * BPL + q, e1 = bins[f + (f >> 5)];
+            big |= (e1 - e0 > kFineOverflow ? 1u : 0u) << q;
+            e0 = e1;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kWBItems; ++j) {
+          if (j * 32 + lane < len) {
+            const uint32_t f = fr[j], b0 = bin_beg(f);
+            if (bins[f + (f >> 5)] - b0 > kFineOverflow && (v[j] ^ flip) != B[b0]) mixed = true;
+          }
+        }
+        mixed = __any_sync(0xffffffffu, mixed);
+      }
+      if (mixed) {
         for (uint32_t i = lane; i < len; i += 32) B[i] ^= flip;
         __syncwarp();
         warp_bitonic_ok<F64>(B, len, lane);
@@ -1921,27 +1943,41 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
         // key moves at most (its bin's load - 1) places.  The last two keys of the sorted
         // prefix stay in registers (pp <= prev), so a key that moves by at most one place
         // (nearly all of them) costs no branch; only a key below both walks the prefix.
-        if (lo < hi) {
-          uint64_t* q = B + lo;  // q[1] is the key being inserted
-          uint64_t prev = q[0], pp = 0ull, nx = q[1];
-#pragma unroll 2
-          for (uint32_t i = lo + 1; i < hi; ++i, ++q) {
-            const uint64_t x = nx;
-            nx = q[2];  // never written while x is inserted (may read 1 slot past the window)
-            const bool lt = x < prev;
-            const uint64_t m = max(pp, x);
-            if (lt) {
-              q[1] = prev;
-              q[0] = m;
-            }
-            if (lt && x < pp) {  // rare: x belongs below pp (q[0] = pp already)
-              uint64_t* r = q - 1;
-              while (r > B + lo && r[-1] > x) { r[0] = r[-1]; --r; }
-              r[0] = x;
-            }
-            pp = lt ? m : prev;
-            prev = lt ? prev : x;
+        // Bins above kFineOverflow keys hold one value each here (duplicates) and are skipped:
+        // the range is cut at their bounds and each piece is sorted alone.
+        uint32_t s0 = lo, msk = big;
+        while (true) {
+          uint32_t s1 = hi, nxt = 0;
+          if (msk) {  // next duplicate-only big bin: sort up to it, resume after it
+            const uint32_t f = lane * BPL + (__ffs(msk) - 1);
+            s1 = bin_beg(f);
+            nxt = bins[f + (f >> 5)];
           }
+          if (s0 + 1 < s1) {
+            uint64_t* q = B + s0;  // q[1] is the key being inserted
+            uint64_t prev = q[0], pp = 0ull, nx = q[1];
+#pragma unroll 2
+            for (uint32_t i = s0 + 1; i < s1; ++i, ++q) {
+              const uint64_t x = nx;
+              nx = q[2];  // never written while x is inserted (may read past the piece)
+              const bool lt = x < prev;
+              const uint64_t m = max(pp, x);
+              if (lt) {
+                q[1] = prev;
+                q[0] = m;
+              }
+              if (lt && x < pp) {  // rare: x belongs below pp (q[0] = pp already)
+                uint64_t* r = q - 1;
+                while (r > B + s0 && r[-1] > x) { r[0] = r[-1]; --r; }
+                r[0] = x;
+              }
+              pp = lt ? m : prev;
+              prev = lt ? prev : x;
+            }
+          }
+          if (!msk) break;
+          msk &= msk - 1;
+          s0 = nxt;
         }
         oflip = flip;
         OUT = B;

@@ -44,6 +44,56 @@ CONFIGS = {
 }
 
 
+# The paper's nine synthetic workloads, for the widening runs (SURVEY §8(f)
+# NEXT #4): same draws at any size, PCG64(seed).  Readings where the paper is silent
+# (DESIGN.md §4): Zipf(0.75) is drawn over the ranks 1..10^6 (float64 ranks); Root Dups and
+# Two Dups keep the paper's index order (no shuffle); Mix Gauss uses C5's parameters.
+PAPER_WORKLOADS = {
+    "uniform": ("f64", "Uniform(0, N) float64 (P:604-606)"),
+    "normal": ("f64", "Normal(0, 1) float64 (P:608-610)"),
+    "lognormal": ("f64", "LogNormal(0, 0.5) float64 (P:612-614)"),
+    "mixgauss": ("f64", "5-Gaussian mixture float64, C5 parameters (P:616-617)"),
+    "exponential": ("f64", "Exponential(lambda = 2) float64 (P:619-620)"),
+    "chisquared": ("f64", "Chi-squared(k = 4) float64 (P:621-622)"),
+    "rootdups": ("u64", "A[i] = i mod floor(sqrt N) uint64, index order (P:625-626)"),
+    "twodups": ("u64", "A[i] = (i^2 + N/2) mod N uint64, index order (P:627-628)"),
+    "zipf": ("f64", "Zipf(s = 0.75) ranks 1..10^6 float64 (P:629-630)"),
+}
+
+
+def paper_workload(name: str, n: int, seed: int = 7) -> np.ndarray:
+    g = np.random.Generator(np.random.PCG64(seed))
+    if name == "uniform":
+        return g.uniform(0.0, float(n), n)
+    if name == "normal":
+        return g.normal(0.0, 1.0, n)
+    if name == "lognormal":
+        return g.lognormal(0.0, 0.5, n)
+    if name == "mixgauss":
+        c = g.choice(5, size=n, p=[0.3, 0.2, 0.2, 0.2, 0.1])
+        mu = np.array([0.0, 10.0, 20.0, 40.0, 80.0])
+        sd = np.array([1.0, 0.5, 2.0, 0.1, 5.0])
+        return g.normal(mu[c], sd[c])
+    if name == "exponential":
+        return g.exponential(0.5, n)
+    if name == "chisquared":
+        return g.chisquare(4.0, n)
+    if name == "rootdups":
+        r = max(1, int(np.floor(np.sqrt(n))))
+        while r * r > n:
+            r -= 1
+        return np.arange(n, dtype=np.uint64) % np.uint64(max(r, 1))
+    if name == "twodups":
+        i = np.arange(n, dtype=np.uint64)
+        return (i * i + np.uint64(n // 2)) % np.uint64(max(n, 1))
+    if name == "zipf":
+        ranks = np.arange(1, 10**6 + 1, dtype=np.float64)
+        cdf = np.cumsum(ranks ** -0.75)
+        cdf /= cdf[-1]
+        return (np.searchsorted(cdf, g.random(n), side="right") + 1).astype(np.float64)
+    raise KeyError(name)
+
+
 def generate(name: str, n: int | None = None) -> np.ndarray:
     """Exact BASELINE generator call order; ``n`` overrides the size (same distribution)."""
     cfg = CONFIGS[name]

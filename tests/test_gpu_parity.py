@@ -201,6 +201,20 @@ def test_base_case_stress_parity(ipls, kind, n, k):
     assert host(t, a.dtype).tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("name", list(datagen.PAPER_WORKLOADS))
+@pytest.mark.parametrize("n,k", [(300_000, 1024), (1_000_003, 256)])
+def test_paper_workloads_parity(ipls, name, n, k):
+    """The paper's nine synthetic workloads: models, counts,
+    samples at every level and the final array, bit-exact against the oracle."""
+    a = datagen.paper_workload(name, n)
+    want = a.copy()
+    ores = oracle.sort(want, k=k, base_case=4096, trace=True)
+    t = dev(a)
+    gtr = ipls.sort_trace(t, k=k, base_case=4096, key_type=kt_of(a))
+    assert host(t, a.dtype).tobytes() == want.tobytes()
+    compare_traces(gtr, ores)
+
+
 def test_worked_example_sort(ipls, golden):
     x = np.array([float(v) for v in golden("worked_example.txt")["input"][0]])
     t = dev(x)

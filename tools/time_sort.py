@@ -11,8 +11,12 @@ if os.environ.get("IPLS_LIB"):  # A/B a variant build
 names = sys.argv[1:] or ["C2"]
 reps = int(os.environ.get("REPS", "8"))
 for name in names:
-    cfg = datagen.CONFIGS[name]
-    a = datagen.generate(name)
+    if name.startswith("P:"):  # a paper workload (datagen.PAPER_WORKLOADS) at 1e8, C2's k and B
+        cfg = datagen.CONFIGS["C2"]
+        a = datagen.paper_workload(name[2:], int(os.environ.get("N", "100000000")))
+    else:
+        cfg = datagen.CONFIGS[name]
+        a = datagen.generate(name)
     kt = 0 if a.dtype == np.float64 else 1
     src = torch.from_numpy(a.view(np.int64)).cuda()
     t = torch.empty_like(src)
