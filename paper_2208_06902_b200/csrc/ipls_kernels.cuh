@@ -1553,7 +1553,7 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
   }
   __syncthreads();
   BASE_TICK(4);
-  uint32_t fs[ITEMS];  // fine bin | smem slot << 16
+  uint32_t fs[ITEMS];  // fine bin
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     fs[j] = 0;
@@ -1591,46 +1591,94 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
   }
   const bool overflow = __syncthreads_or(mxc > kFineOverflow) != 0;
   BASE_TICK(6);
+  if (overflow) {
+    // An overflowing fine bin that holds one value (duplicates) needs no sorting: every key
+    // of a big bin is compared with one of them, stored at the bin's first slot.  Only bins
+    // of different keys send the window to the bitonic fallback.
+    constexpr uint32_t NB = NT * ITEMS;
+    auto big_start = [&](uint32_t f) -> uint32_t {  // start of bin f if it is big, else ~0
+      const uint32_t st = fh[f], en = f + 1 < NB ? fh[f + 1] : len;
+      return en - st > kFineOverflow ? st : ~0u;
+    };
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j)
+      if (j * NT + threadIdx.x < len) {
+        const uint32_t st = big_start(fs[j]);
+        if (st != ~0u) B[st] = v[j];
+      }
+    __syncthreads();
+    bool mixed = false;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j)
+      if (j * NT + threadIdx.x < len) {
+        const uint32_t st = big_start(fs[j]);
+        if (st != ~0u && B[st] != v[j]) mixed = true;
+      }
+    if (__syncthreads_or(mixed)) {
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j)
+        if (j * NT + threadIdx.x < len) B[j * NT + threadIdx.x] = v[j];
+      bitonic_sort_smem<NT>(B, len);
+      return B;
+    }
+  }
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     if (j * NT + threadIdx.x < len) {
-      const uint32_t slot = atomicAdd(&fh[fs[j]], 1u);
-      B[slot] = v[j];
-      fs[j] |= slot << 16;
+      B[atomicAdd(&fh[fs[j]], 1u)] = v[j];
     }
   }
   __syncthreads();
   BASE_TICK(7);
+  // fine bin f occupies B[f ? fh[f - 1] : 0, fh[f]) now.
+  uint32_t big = 0;  // this thread's fine bins above kFineOverflow keys (one value each)
   if (overflow) {
-    bitonic_sort_smem<NT>(B, len);
-    return B;
+    uint32_t e0 = lo;
+    for (int q = 0; q < ITEMS; ++q) {
+      const uint32_t e1 = fh[threadIdx.x * ITEMS + q];
+      big |= (e1 - e0 > kFineOverflow ? 1u : 0u) << q;
+      e0 = e1;
+    }
   }
   // B is ordered across fine bins: every thread insertion-sorts its range B[lo, hi) (only
-  // in-bin inversions move; each key moves at most its bin's load - 1 places).
-  // The last two keys of the sorted prefix stay in registers (pp <= prev): a key that moves by
-  // at most one place costs no branch; only a key below both walks the prefix.
-  if (lo < hi) {
-    uint64_t* q = B + lo;  // q[1] is the key being inserted
-    uint64_t prev = q[0], pp = 0ull, nx = (lo + 1 < hi) ? q[1] : 0ull;
-    for (uint32_t i = lo + 1; i < hi; ++i, ++q) {
-      const uint64_t x = nx;
-      nx = (i + 1 < hi) ? q[2] : 0ull;  // never written while x is inserted
-      if (x < prev) {
-        q[1] = prev;
-        if (x >= pp) {
-          q[0] = x;
-          pp = x;
-        } else {  // rare: x belongs below pp
-          q[0] = pp;
-          uint64_t* r = q - 1;
-          while (r > B + lo && r[-1] > x) { r[0] = r[-1]; --r; }
-          r[0] = x;
+  // in-bin inversions move; each key moves at most its bin's load - 1 places), cut around
+  // its duplicate-only big bins.  The last two keys of the sorted prefix stay in registers
+  // (pp <= prev): a key that moves by at most one place costs no branch; only a key below
+  // both walks the prefix.
+  uint32_t s0 = lo, msk = big;
+  while (true) {
+    uint32_t s1 = hi, nxt = 0;
+    if (msk) {
+      const uint32_t f = threadIdx.x * ITEMS + (__ffs(msk) - 1);
+      s1 = f ? fh[f - 1] : 0u;
+      nxt = fh[f];
+    }
+    if (s0 + 1 < s1) {
+      uint64_t* q = B + s0;  // q[1] is the key being inserted
+      uint64_t prev = q[0], pp = 0ull, nx = q[1];
+      for (uint32_t i = s0 + 1; i < s1; ++i, ++q) {
+        const uint64_t x = nx;
+        nx = (i + 1 < s1) ? q[2] : 0ull;  // never written while x is inserted
+        if (x < prev) {
+          q[1] = prev;
+          if (x >= pp) {
+            q[0] = x;
+            pp = x;
+          } else {  // rare: x belongs below pp
+            q[0] = pp;
+            uint64_t* r = q - 1;
+            while (r > B + s0 && r[-1] > x) { r[0] = r[-1]; --r; }
+            r[0] = x;
+          }
+        } else {
+          pp = prev;
+          prev = x;
         }
-      } else {
-        pp = prev;
-        prev = x;
       }
     }
+    if (!msk) break;
+    msk &= msk - 1;
+    s0 = nxt;
   }
   __syncthreads();
   BASE_TICK(8);
