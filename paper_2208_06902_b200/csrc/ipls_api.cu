@@ -293,6 +293,8 @@ void set_attrs() {
                           (int)fit_smem(kFitMaxS)));
   ck(cudaFuncSetAttribute(k_fit_small<F64, kFSThreads, kFSItems>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSSmem));
+  ck(cudaFuncSetAttribute(k_fit_small<F64, kFSThreads, kFMItems>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFMSmem));
   ck(cudaFuncSetAttribute(k_fit_small<F64, kFLThreads, kFLItems>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFLSmem));
   ck(cudaFuncSetAttribute(k_base_sort<F64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -400,7 +402,10 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
       IPLS_PROF("gather_fit", 0);
       const uint32_t cap = fit_cap(max_S);
       uint32_t* redo = at<uint32_t>(meta, ML.seg_term);  // scratch until K2 writes seg_term
-      if (max_S <= (uint32_t)kFSMax)
+      if (max_S <= (uint32_t)kFMMax)
+        k_fit_small<F64, kFSThreads, kFMItems><<<nseg, kFSThreads, kFMSmem, st>>>(
+            src, segs, seed, level, k, trace ? samples : nullptr, models, redo);
+      else if (max_S <= (uint32_t)kFSMax)
         k_fit_small<F64, kFSThreads, kFSItems><<<nseg, kFSThreads, kFSSmem, st>>>(
             src, segs, seed, level, k, trace ? samples : nullptr, models, redo);
       else

@@ -338,6 +338,11 @@ constexpr int kFSThreads = 256;
 constexpr int kFSItems = 20;                     // samples per thread
 constexpr int kFSMax = kFSThreads * kFSItems;    // 5120 (S(m) for m <= 2^25 at k = 1024)
 constexpr size_t kFSSmem = (size_t)kFSMax * 12;
+// 16 samples per thread for samples of <= 4096 keys (S(m) for m <= 2^20 at k = 1024): fewer
+// registers than the 20-sample variant (no spills), same 3 CTAs per SM
+constexpr int kFMItems = 16;
+constexpr int kFMMax = kFSThreads * kFMItems;
+constexpr size_t kFMSmem = (size_t)kFMMax * 12;
 // Large-sample variant (one CTA of 1024 threads, 8 samples each: every S(m) <= 7k - 1 < 8192),
 // used for the levels whose largest sample exceeds kFSMax (level 0 at >= 2^25 keys).
 constexpr int kFLThreads = 1024;
@@ -512,9 +517,33 @@ __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
         f4[q] = o;
       }
     }
-    if (__syncthreads_or(!exact && mxc > kFineOverflow)) {
-      if (threadIdx.x == 0) redo[blockIdx.x] = 1u;  // the 1024-thread kernel sorts it
-      return;
+    const bool ovf = __syncthreads_or(!exact && mxc > kFineOverflow) != 0;
+    if (ovf) {
+      // A fine bin above kFineOverflow keys that holds one value (duplicate-heavy samples)
+      // needs no sorting: every key of a big bin is compared with one of them, stored at the
+      // bin's first slot.  Bins of different keys go to the 1024-thread kernel (bitonic).
+      auto big_start = [&](uint32_t fb) -> uint32_t {
+        const uint32_t st = fh[fb], en = fb + 1 < (uint32_t)SMAX ? fh[fb + 1] : S;
+        return en - st > kFineOverflow ? st : ~0u;
+      };
+#pragma unroll
+      for (int r = 0; r < IT; ++r)
+        if (r * NT + threadIdx.x < S) {
+          const uint32_t st = big_start(f[r]);
+          if (st != ~0u) B[st] = v[r];
+        }
+      __syncthreads();
+      bool mixed = false;
+#pragma unroll
+      for (int r = 0; r < IT; ++r)
+        if (r * NT + threadIdx.x < S) {
+          const uint32_t st = big_start(f[r]);
+          if (st != ~0u && B[st] != v[r]) mixed = true;
+        }
+      if (__syncthreads_or(mixed)) {
+        if (threadIdx.x == 0) redo[blockIdx.x] = 1u;  // the 1024-thread kernel sorts it
+        return;
+      }
     }
 #pragma unroll
     for (int r = 0; r < IT; ++r)
@@ -522,15 +551,30 @@ __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
     __syncthreads();
     FITL_TICK(26);
     if (!exact) {
+      // every thread insertion-sorts the range of its fine bins [IT t, IT t + IT) (keys of
+      // different bins are already ordered); with big bins (duplicates only) the range is
+      // sorted one bin at a time and the big bins are skipped
       const uint32_t f0 = threadIdx.x * IT;
       const uint32_t beg = f0 ? fh[f0 - 1] : 0u, end = fh[f0 + IT - 1];
-      for (uint32_t i = beg + 1; i < end; ++i) {
-        const uint64_t x = B[i];
-        uint64_t y = B[i - 1];
-        if (y <= x) continue;
-        uint32_t j = i;
-        do { B[j] = y; --j; } while (j > beg && (y = B[j - 1]) > x);
-        B[j] = x;
+      auto insertion = [&](uint32_t b0, uint32_t b1) {
+        for (uint32_t i = b0 + 1; i < b1; ++i) {
+          const uint64_t x = B[i];
+          uint64_t y = B[i - 1];
+          if (y <= x) continue;
+          uint32_t j = i;
+          do { B[j] = y; --j; } while (j > b0 && (y = B[j - 1]) > x);
+          B[j] = x;
+        }
+      };
+      if (!ovf) {
+        insertion(beg, end);
+      } else {
+        uint32_t b0 = beg;
+        for (int qb = 0; qb < IT; ++qb) {
+          const uint32_t b1 = fh[f0 + qb];
+          if (b1 - b0 <= kFineOverflow) insertion(b0, b1);
+          b0 = b1;
+        }
       }
     }
   }
