@@ -1929,10 +1929,18 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       }
       range = (double)(umx - umn);
     }
-    const uint64_t* OUT = K;  // constant (u64) windows are already sorted
+    const uint64_t* OUT = K;  // constant windows (one bit pattern) are already sorted
     uint64_t oflip = 0;       // OUT holds bits ^ oflip
     WB_TICK(2);
-    if (!F64 && umn == umx) {
+    bool constant = !F64 && umn == umx;
+    if (F64 && range == 0.0) {  // one value, but it may mix -0.0 and +0.0: compare the bits
+      const uint64_t v00 = __shfl_sync(0xffffffffu, v[0], 0);  // every lane (not short-circuited)
+      bool same = true;
+#pragma unroll
+      for (int j = 0; j < kWBItems; ++j) same &= v[j] == v00;
+      constant = __all_sync(0xffffffffu, same);
+    }
+    if (constant) {
       // nothing to sort
     } else if (!(range > 0.0) || !(range < 1.79e308)) {  // zero inside, infinities, overflow
       __syncwarp();  // every lane holds its keys: B may overwrite K
