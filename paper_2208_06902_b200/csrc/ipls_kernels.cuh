@@ -1332,7 +1332,7 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
 // Terminal segments (every child <= base case): the children are sorted by the base case
 // right after this level, so the scatter does not need stable ranks.  Per tile: bucket counts
 // (smem atomics), a scan over buckets, placement by an atomic cursor per bucket, write-out as
-// in the stable path.  No per-warp counters, no cross-warp scan, no stability check; no
+// in the stable path (the staged key's bucket is recomputed there rather than staged).  No per-warp counters, no cross-warp scan, no stability check; no
 // homogeneity tracking either (only children above the base case can be homogeneous-final).
 // Tiles are twice as long as the stable path's (16 keys per thread): half the barriers and
 // scans per key, and bucket runs twice as long per tile (fuller L2 lines per write-out).
@@ -1342,7 +1342,7 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
 constexpr int kURounds = IPLS_UROUNDS;             // keys per thread per tile
 constexpr int kUTile = kSThreads4 * kURounds;      // 16384
 __host__ __device__ constexpr size_t scatter_unstable_smem_bytes(uint32_t k) {
-  return (size_t)kUTile * 8 + (size_t)k * 8 * 2 + (size_t)k * 4 * 2 + (size_t)kUTile * 2;
+  return (size_t)kUTile * 8 + (size_t)k * 8 * 2 + (size_t)k * 4 * 2;
 }
 
 template <bool F64, bool EQ3>
@@ -1357,7 +1357,6 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
   uint64_t* adj = runa + k;                                       // k
   uint32_t* cnt = reinterpret_cast<uint32_t*>(adj + k);           // k
   uint32_t* cur = cnt + k;                                        // k
-  uint16_t* sbk = reinterpret_cast<uint16_t*>(cur + k);           // kUTile
   __shared__ uint32_t s_warp[40];
   const Bucketer<F64, EQ3> bucket(md, k);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
@@ -1425,9 +1424,7 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
     for (int r = 0; r < kURounds; ++r) {
       const uint32_t bb = (bk[r >> 1] >> (16 * (r & 1))) & 0xffffu;
       if (bb != 0xffffu) {
-        const uint32_t pos = atomicAdd(&cur[bb], 1u);
-        stage[pos] = key[r];
-        sbk[pos] = (uint16_t)bb;
+        stage[atomicAdd(&cur[bb], 1u)] = key[r];
       }
     }
 #pragma unroll
@@ -1437,8 +1434,12 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
     }
     __syncthreads();
     SC_TICK(14);
-    for (uint32_t q = threadIdx.x; q < tl; q += NT)
-      st_evict_last(reinterpret_cast<uint64_t*>(adj[sbk[q]]) + q, stage[q]);
+    // the bucket of a staged key is recomputed (same arithmetic, so the same bucket): cheaper
+    // than a random 2-byte smem store in the placement and a load here
+    for (uint32_t q = threadIdx.x; q < tl; q += NT) {
+      const uint64_t x = stage[q];
+      st_evict_last(reinterpret_cast<uint64_t*>(adj[bucket(x)]) + q, x);
+    }
     __syncthreads();
     SC_TICK(7);
   }
