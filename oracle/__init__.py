@@ -39,6 +39,7 @@ KEY_F64 = 0
 KEY_U64 = 1
 MODEL_LINEAR = 0
 MODEL_EQ3 = 1
+MODEL_TREE = 2
 DEFAULT_SEED = 0x49504C53  # "IPLS"
 
 
@@ -93,6 +94,11 @@ def lib():
         L.oracle_trace_num_levels.argtypes = [vp]; L.oracle_trace_num_levels.restype = u32
         L.oracle_trace_snapshot.argtypes = [vp, u32]; L.oracle_trace_snapshot.restype = vp
         L.oracle_sort.argtypes = [vp, sz, i32, u32, u32, u64, vp]; L.oracle_sort.restype = i32
+        L.oracle_sort_model.argtypes = [vp, sz, i32, u32, u32, u64, i32, vp]
+        L.oracle_sort_model.restype = i32
+        L.oracle_tree_splitters.argtypes = [vp, sz, u32, i32, vp]
+        L.oracle_tree_splitters.restype = None
+        L.oracle_tree_bucket.argtypes = [u64, i32, vp, u32]; L.oracle_tree_bucket.restype = u32
         _lib = L
     return _lib
 
@@ -212,16 +218,34 @@ class SortResult:
     snapshots: List[np.ndarray]
 
 
+def tree_splitters(sorted_keys: np.ndarray, k: int) -> np.ndarray:
+    """R22: the k-1 equidistant order statistics of a sorted sample, as ordering keys."""
+    a = np.ascontiguousarray(sorted_keys)
+    out = np.zeros(k - 1, np.uint64)
+    lib().oracle_tree_splitters(_ptr(a), a.size, k, _key_type(a), _ptr(out))
+    return out
+
+
+def tree_bucket(x, spl_ok: np.ndarray, k: int) -> int:
+    """R23: leaf of the splitter tree for one key (float64 or uint64 scalar)."""
+    a = np.asarray([x])
+    if a.dtype not in (np.float64, np.uint64):
+        a = a.astype(np.float64)
+    s = np.ascontiguousarray(spl_ok, dtype=np.uint64)
+    return int(lib().oracle_tree_bucket(int(a.view(np.uint64)[0]), _key_type(a), _ptr(s), k))
+
+
 def sort(keys: np.ndarray, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SEED,
-         trace: bool = False, snapshots: bool = False) -> SortResult:
-    """Sort ``keys`` (float64 or uint64 numpy array) IN PLACE with the oracle."""
+         trace: bool = False, snapshots: bool = False, model: int = MODEL_LINEAR) -> SortResult:
+    """Sort ``keys`` (float64 or uint64 numpy array) IN PLACE with the oracle; ``model``
+    MODEL_LINEAR (FMCD, IPLS) or MODEL_TREE (splitter tree, IPS4o's classifier)."""
     if not keys.flags.c_contiguous:
         raise ValueError("keys must be C-contiguous")
     kt = _key_type(keys)
     L = lib()
     tr = L.oracle_trace_new(1 if snapshots else 0) if (trace or snapshots) else None
     try:
-        st = L.oracle_sort(_ptr(keys), keys.size, kt, k, base_case, seed, tr)
+        st = L.oracle_sort_model(_ptr(keys), keys.size, kt, k, base_case, seed, model, tr)
         recs: List[Record] = []
         snaps: List[np.ndarray] = []
         levels = 0

@@ -65,10 +65,17 @@ struct Model {
   uint32_t k;
   uint32_t D, capped;
   uint64_t pivot_ok;
+  const uint64_t* spl = nullptr;  /* TREE: k-1 sorted splitters (ordering keys) */
 };
+
+/* R23: leaf of the descent j <- 2j + (x > a_j) = number of splitters strictly below x. */
+uint32_t tree_bucket_of(uint64_t o, const uint64_t* spl, uint32_t k) {
+  return (uint32_t)(std::lower_bound(spl, spl + (k - 1), o) - spl);
+}
 
 /* P:394-402 with R7: y = RN(RN(A*v) + B); 0 if !(y >= 0); k-1 if y >= k; else floor(y). */
 uint32_t bucket_of(uint64_t bits, int key_type, const Model& md) {
+  if (md.kind == ORACLE_MODEL_TREE) return tree_bucket_of(ok_of(bits, key_type), md.spl, md.k);
   if (md.kind == ORACLE_MODEL_EQ3) {
     uint64_t o = ok_of(bits, key_type);
     if (o < md.pivot_ok) return 0;
@@ -166,11 +173,35 @@ uint32_t oracle_bucket(uint64_t bits, int key_type, int kind, double A, double B
   return bucket_of(bits, key_type, md);
 }
 
+void oracle_tree_splitters(const uint64_t* sorted_bits, size_t S, uint32_t k, int key_type,
+                           uint64_t* spl_ok) {
+  /* R22: equidistant order statistics of the sorted sample. */
+  for (uint32_t i = 1; i < k; ++i)
+    spl_ok[i - 1] = ok_of(sorted_bits[(size_t)(((unsigned __int128)i * S) / k)], key_type);
+}
+
+uint32_t oracle_tree_bucket(uint64_t bits, int key_type, const uint64_t* spl_ok, uint32_t k) {
+  return tree_bucket_of(ok_of(bits, key_type), spl_ok, k);
+}
+
+namespace {
+void partition_model(const uint64_t* in, uint64_t* out, size_t n, int key_type, const Model& md,
+                     uint64_t* offsets, uint16_t* ids);
+}
+
 void oracle_partition(const uint64_t* in, uint64_t* out, size_t n, int key_type, int kind,
                       double A, double B, uint32_t k, uint64_t pivot_ok, uint64_t* offsets,
                       uint16_t* ids) {
-  /* Counting sort by bucket, stable (P:505-530; R11). */
   Model md{kind, A, B, k, 0, 0, pivot_ok};
+  partition_model(in, out, n, key_type, md, offsets, ids);
+}
+
+namespace {
+void partition_model(const uint64_t* in, uint64_t* out, size_t n, int key_type, const Model& md,
+                     uint64_t* offsets, uint16_t* ids) {
+  /* Counting sort by bucket, stable (P:505-530; R11). */
+  const int kind = md.kind;
+  const uint32_t k = md.k;
   uint32_t ke = (kind == ORACLE_MODEL_EQ3) ? 3 : k;
   std::vector<uint32_t> b(n);
   std::vector<uint64_t> cnt(ke, 0);
@@ -185,6 +216,7 @@ void oracle_partition(const uint64_t* in, uint64_t* out, size_t n, int key_type,
     for (uint32_t j = 0; j <= ke; ++j) offsets[j] = pos[j];
   for (size_t i = 0; i < n; ++i) out[pos[b[i]]++] = in[i];
 }
+}  // namespace
 
 oracle_trace* oracle_trace_new(int keep_snapshots) {
   oracle_trace* t = new oracle_trace();
@@ -203,7 +235,14 @@ const uint64_t* oracle_trace_snapshot(const oracle_trace* t, uint32_t level) {
 
 int oracle_sort(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32_t base_case,
                 uint64_t seed, oracle_trace* trace) {
+  return oracle_sort_model(keys, n, key_type, k, base_case, seed, ORACLE_MODEL_LINEAR, trace);
+}
+
+int oracle_sort_model(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32_t base_case,
+                      uint64_t seed, int model, oracle_trace* trace) {
   if (k < 3 || k > 65535) return 1;
+  if (model != ORACLE_MODEL_LINEAR && model != ORACLE_MODEL_TREE) return 1;
+  if (model == ORACLE_MODEL_TREE && (k < 4 || (k & (k - 1)) != 0)) return 1;
   if (key_type != ORACLE_KEY_F64 && key_type != ORACLE_KEY_U64) return 1;
   if (n > 0 && keys == nullptr) return 1;
   /* Ingest: reject NaN before any write (R0). */
@@ -234,10 +273,17 @@ int oracle_sort(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32_t bas
       std::sort(smp.begin(), smp.end(), [&](uint64_t x, uint64_t y) {
         return ok_of(x, key_type) < ok_of(y, key_type);
       });
-      /* Phase 3: train (Listing 1) or fall back to the equality split (R5, R10, R19). */
+      /* Phase 3: train (Listing 1) or fall back to the equality split (R5, R10, R19);
+       * with the tree model, pick the splitters (R22). */
       Model md{ORACLE_MODEL_LINEAR, 0.0, 0.0, k, 0, 0, 0};
+      std::vector<uint64_t> spl;
       bool eq3 = sg.force_eq3 || S < 4;
-      if (!eq3) {
+      if (!eq3 && model == ORACLE_MODEL_TREE) {
+        spl.resize(k - 1);
+        oracle_tree_splitters(smp.data(), S, k, key_type, spl.data());
+        md.kind = ORACLE_MODEL_TREE;
+        md.spl = spl.data();
+      } else if (!eq3) {
         std::vector<double> sv(S);
         for (uint64_t j = 0; j < S; ++j) sv[j] = value_of(smp[j], key_type);
         int deg = oracle_fit_fmcd(sv.data(), S, k, &md.A, &md.B, &md.D, &md.capped);
@@ -251,8 +297,7 @@ int oracle_sort(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32_t bas
       const uint32_t ke = eq3 ? 3 : k;
       /* Phase 4: predict every key, then move keys into contiguous buckets (stable). */
       std::vector<uint64_t> off(ke + 1);
-      oracle_partition(a, tmp.data(), m, key_type, md.kind, md.A, md.B, md.k, md.pivot_ok,
-                       off.data(), nullptr);
+      partition_model(a, tmp.data(), m, key_type, md, off.data(), nullptr);
       std::memcpy(a, tmp.data(), m * 8);
 
       if (trace) {
@@ -264,14 +309,15 @@ int oracle_sort(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32_t bas
         for (uint32_t j = 0; j < ke; ++j) c[j] = off[j + 1] - off[j];
         r.requeued = 0;
         for (uint32_t j = 0; j < ke; ++j)
-          if (md.kind == ORACLE_MODEL_LINEAR && c[j] == m) r.requeued = 1;
+          if (md.kind != ORACLE_MODEL_EQ3 && c[j] == m) r.requeued = 1;
         trace->recs.push_back(r);
         trace->samples.push_back(smp);
         trace->counts.push_back(c);
       }
-      /* No-progress guard (R10): a linear model that kept every key in one bucket. */
+      /* No-progress guard (R10, R24): a linear or tree model that kept every key in one
+       * bucket. */
       bool stuck = false;
-      if (md.kind == ORACLE_MODEL_LINEAR)
+      if (md.kind != ORACLE_MODEL_EQ3)
         for (uint32_t j = 0; j < ke; ++j)
           if (off[j + 1] - off[j] == m) stuck = true;
       if (stuck) {

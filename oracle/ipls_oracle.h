@@ -23,7 +23,7 @@ extern "C" {
 #endif
 
 enum { ORACLE_KEY_F64 = 0, ORACLE_KEY_U64 = 1 };
-enum { ORACLE_MODEL_LINEAR = 0, ORACLE_MODEL_EQ3 = 1 };
+enum { ORACLE_MODEL_LINEAR = 0, ORACLE_MODEL_EQ3 = 1, ORACLE_MODEL_TREE = 2 };
 
 /* Order-preserving key ("extractor ... maps double to integers"). */
 uint64_t oracle_ordering_key(uint64_t bits, int key_type);
@@ -54,6 +54,17 @@ void oracle_partition(const uint64_t* in, uint64_t* out, size_t n, int key_type,
                       double A, double B, uint32_t k, uint64_t pivot_ok, uint64_t* offsets,
                       uint16_t* ids);
 
+/* Splitter-tree model (IPS4o's decision tree; DESIGN.md
+ * R22-R24): the k-1 splitters are the equidistant order statistics s[floor(i S / k)],
+ * i = 1..k-1, of the sorted sample (k a power of two), as ordering keys.  spl_ok: k-1
+ * entries, nondecreasing. */
+void oracle_tree_splitters(const uint64_t* sorted_bits, size_t S, uint32_t k, int key_type,
+                           uint64_t* spl_ok);
+/* Bucket of one key under the tree: the branchless descent j <- 2j + (x > a_j) over the
+ * implicit tree of the splitters ends at leaf #{i : spl_i < ok(x)} (ties go left, R23),
+ * which is what this returns (the plain definition, by binary search). */
+uint32_t oracle_tree_bucket(uint64_t bits, int key_type, const uint64_t* spl_ok, uint32_t k);
+
 /* One record per partitioned segment, in level order then increasing begin. */
 typedef struct {
   uint32_t level, kind;
@@ -83,6 +94,10 @@ const uint64_t* oracle_trace_snapshot(const oracle_trace* t, uint32_t level);
  * unmodified), or 1 on invalid arguments. */
 int oracle_sort(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32_t base_case,
                 uint64_t seed, oracle_trace* trace);
+/* Same with the model chosen: ORACLE_MODEL_LINEAR (FMCD, the paper's IPLS) or
+ * ORACLE_MODEL_TREE (splitter tree, IPS4o's classifier; k must be a power of two >= 4). */
+int oracle_sort_model(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32_t base_case,
+                      uint64_t seed, int model, oracle_trace* trace);
 
 #ifdef __cplusplus
 }
