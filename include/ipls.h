@@ -43,7 +43,14 @@ typedef enum { IPLS_KEY_F64 = 0, IPLS_KEY_U64 = 1 } ipls_key_type;
 /* Partition model kinds.  LINEAR: F(x) = clamp(floor(a*x + b), 0, k-1) with
  * (a, b) from FMCD (Listing 1).  EQ3: equality split into <pivot, ==pivot,
  * >pivot by ordering key (IPS4o equality buckets; used for degenerate samples, R5). */
-typedef enum { IPLS_MODEL_LINEAR = 0, IPLS_MODEL_EQ3 = 1 } ipls_model_kind;
+typedef enum { IPLS_MODEL_LINEAR = 0, IPLS_MODEL_EQ3 = 1, IPLS_MODEL_TREE = 2 } ipls_model_kind;
+
+/* ipls_config.flags.  IPLS_FLAG_TREE_MODEL: classify with IPS4o's splitter tree (
+ * SURVEY §8(f) NEXT #2; R22-R24) instead of the FMCD linear model: the k-1
+ * splitters are the equidistant order statistics of the same sorted sample, and every key
+ * descends j <- 2j + (x > a_j) (ties left).  k must be a power of two.  Degenerate cases
+ * and the no-progress guard are the same (EQ3).  Trace records carry kind IPLS_MODEL_TREE. */
+#define IPLS_FLAG_TREE_MODEL 1u
 
 #define IPLS_MAX_K 1024u          /* fan-out limit of the sm_100a kernels (smem-resident) */
 #define IPLS_MAX_BASE_CASE 4096u  /* base-case limit (n <= 2^12)                    */
@@ -53,7 +60,7 @@ typedef struct {
   uint32_t k;         /* buckets per level, 3..IPLS_MAX_K (P:473 uses 256)                 */
   uint32_t base_case; /* segments of <= base_case keys go to the base case, 1..4096 */
   uint64_t seed;      /* sampling seed (R18)                                               */
-  uint32_t flags;     /* reserved, must be 0                                               */
+  uint32_t flags;     /* 0 or IPLS_FLAG_TREE_MODEL (k a power of two); other bits: invalid  */
 } ipls_config;
 
 typedef struct {

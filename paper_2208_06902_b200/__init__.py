@@ -17,7 +17,7 @@ import numpy as np
 
 __all__ = [
     "IPLSError", "lib", "sort", "sort_host", "fit_fmcd", "partition_level", "sort_trace",
-    "workspace_bytes", "Model", "Record", "KEY_F64", "KEY_U64", "MODEL_LINEAR", "MODEL_EQ3",
+    "workspace_bytes", "Model", "Record", "KEY_F64", "KEY_U64", "MODEL_LINEAR", "MODEL_EQ3", "MODEL_TREE",
     "DEFAULT_SEED", "launch_count",
 ]
 
@@ -28,6 +28,8 @@ KEY_F64 = 0
 KEY_U64 = 1
 MODEL_LINEAR = 0
 MODEL_EQ3 = 1
+MODEL_TREE = 2        # splitter tree (IPS4o's classifier; config flag FLAG_TREE_MODEL)
+FLAG_TREE_MODEL = 1
 DEFAULT_SEED = 0x49504C53
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "NaN key", 3: "degenerate sample",
@@ -129,8 +131,11 @@ def _check(st: int):
         raise IPLSError(st, extra)
 
 
-def _cfg(k: int, base_case: int, seed: int) -> _Config:
-    return _Config(k, base_case, seed, 0)
+def _cfg(k: int, base_case: int, seed: int, model: int = MODEL_LINEAR) -> _Config:
+    """model: MODEL_LINEAR (FMCD, the paper's IPLS) or MODEL_TREE (splitter tree)."""
+    if model not in (MODEL_LINEAR, MODEL_TREE):
+        raise ValueError("model must be MODEL_LINEAR or MODEL_TREE")
+    return _Config(k, base_case, seed, FLAG_TREE_MODEL if model == MODEL_TREE else 0)
 
 
 def _stream(stream) -> Optional[int]:
@@ -178,11 +183,12 @@ def launch_count() -> int:
 
 
 def sort(keys, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SEED,
-         key_type: Optional[int] = None, stream=None, workspace=None) -> None:
+         key_type: Optional[int] = None, stream=None, workspace=None,
+         model: int = MODEL_LINEAR) -> None:
     """Sort a CUDA tensor in place (float64; uint64 or int64 holding uint64 bits)."""
     _check_tensor(keys)
     kt = _key_type_of(keys, key_type)
-    c = _cfg(k, base_case, seed)
+    c = _cfg(k, base_case, seed, model)
     ws, wsb = (None, 0)
     if workspace is not None:
         ws, wsb = workspace.data_ptr(), workspace.numel() * workspace.element_size()
@@ -190,8 +196,9 @@ def sort(keys, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SEED,
                               _stream(stream)))
 
 
-def workspace_bytes(n: int, key_type: int = KEY_F64, k: int = 256, base_case: int = 4096) -> int:
-    c = _cfg(k, base_case, DEFAULT_SEED)
+def workspace_bytes(n: int, key_type: int = KEY_F64, k: int = 256, base_case: int = 4096,
+                    model: int = MODEL_LINEAR) -> int:
+    c = _cfg(k, base_case, DEFAULT_SEED, model)
     return int(lib().ipls_workspace_bytes(n, key_type, ctypes.byref(c)))
 
 
@@ -282,12 +289,12 @@ class TraceResult:
 def sort_trace(keys, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SEED,
                key_type: Optional[int] = None, snapshot_levels: int = 0, stream=None,
                max_records: int = 1 << 16, max_counts: int = 1 << 24,
-               max_samples: int = 1 << 24) -> TraceResult:
+               max_samples: int = 1 << 24, model: int = MODEL_LINEAR) -> TraceResult:
     """Sort in place and return the per-segment trace (records ordered by level, begin)."""
     import torch
     _check_tensor(keys)
     kt = _key_type_of(keys, key_type)
-    c = _cfg(k, base_case, seed)
+    c = _cfg(k, base_case, seed, model)
     n = keys.numel()
     snaps = None
     if snapshot_levels:

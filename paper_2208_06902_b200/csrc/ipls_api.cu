@@ -111,6 +111,7 @@ struct Params {
   uint64_t n;
   uint32_t k, B, chunk_keys;
   uint32_t cap_segs, cap_chunks, cap_samples, cap_wins, cap_wbig, cap_fills;
+  bool tree;  // IPLS_FLAG_TREE_MODEL: splitter-tree model instead of FMCD
 };
 
 #ifndef IPLS_CHUNK_CAP
@@ -125,9 +126,9 @@ uint32_t pick_chunk_keys(uint64_t n) {
   return (uint32_t)c;
 }
 
-Params make_params(uint64_t n, uint32_t k, uint32_t B) {
+Params make_params(uint64_t n, uint32_t k, uint32_t B, bool tree = false) {
   Params p{};
-  p.n = n; p.k = k; p.B = B;
+  p.n = n; p.k = k; p.B = B; p.tree = tree;
   p.chunk_keys = pick_chunk_keys(n);
   const uint64_t segs = n / ((uint64_t)B + 1) + 2;
   const uint64_t chunks = n / p.chunk_keys + segs + 1;
@@ -177,10 +178,11 @@ FixedLayout fixed_layout(const Params& p) {
 // allocation can be cleared cheaply.
 struct MetaLayout {
   size_t status, cflag, cref, chunk_pre, models, samples, seg_dst, seg_tot, seg_done, seg_term,
-      total;
+      tree, total;
 };
 
-MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_t k) {
+MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_t k,
+                       bool tree = false) {
   MetaLayout L{};
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
@@ -194,12 +196,13 @@ MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_
   L.seg_tot = take(segs * k * 4);
   L.seg_done = take(segs * 4);
   L.seg_term = take(segs * 4);
+  L.tree = take(tree ? segs * kMaxK * 8 : 0);  // splitter heaps (8 KB per segment)
   L.total = o;
   return L;
 }
 
 size_t worst_meta_bytes(const Params& p) {
-  return meta_layout(p.cap_segs, p.cap_chunks, p.cap_samples, p.k).total;
+  return meta_layout(p.cap_segs, p.cap_chunks, p.cap_samples, p.k, p.tree).total;
 }
 
 // Device buffers for one call: either the caller's workspace or the per-stream cache.
@@ -261,12 +264,25 @@ struct TraceSink {
 
 template <bool F64>
 void launch_scatter(uint32_t nchunk, cudaStream_t st, const LevelArgs& la, uint64_t* user,
-                    uint64_t* scr) {
+                    uint64_t* scr, bool tree = false) {
   const size_t smem = std::max(scatter_smem_bytes(la.k), scatter_unstable_smem_bytes(la.k));
-  k_scatter<F64><<<nchunk, kSThreads4, smem, st>>>(la, user, scr);
+  if (tree)
+    k_scatter<F64, true><<<nchunk, kSThreads4, smem, st>>>(la, user, scr);
+  else
+    k_scatter<F64, false><<<nchunk, kSThreads4, smem, st>>>(la, user, scr);
   ck_launch();
 }
+template <bool F64>
+void launch_classify(uint32_t nchunk, cudaStream_t st, const LevelArgs& la, bool tree = false);
 size_t classify_smem(uint32_t k) { return (size_t)k * 4; }
+template <bool F64>
+void launch_classify(uint32_t nchunk, cudaStream_t st, const LevelArgs& la, bool tree) {
+  if (tree)
+    k_classify_scan<F64, true><<<nchunk, kCThreads, classify_smem(la.k), st>>>(la);
+  else
+    k_classify_scan<F64, false><<<nchunk, kCThreads, classify_smem(la.k), st>>>(la);
+  ck_launch();
+}
 size_t warp_base_smem() { return kWBSmemPerWarp * kWBWarps; }
 size_t base_smem() { return kBCSmem; }
 int g_num_sms = 0;
@@ -303,11 +319,15 @@ void set_attrs() {
                           (int)base_smem()));
   ck(cudaFuncSetAttribute(k_base_warp<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)warp_base_smem()));
-  ck(cudaFuncSetAttribute(k_classify_scan<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)classify_smem(kMaxK)));
-  ck(cudaFuncSetAttribute(k_scatter<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)std::max({scatter_smem_bytes(kMaxK), scatter_unstable_smem_bytes(kMaxK),
-                                         win_scratch_bytes(kMaxK)})));
+  for (int tr = 0; tr < 2; ++tr) {
+    ck(cudaFuncSetAttribute(tr ? k_classify_scan<F64, true> : k_classify_scan<F64, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)classify_smem(kMaxK)));
+    ck(cudaFuncSetAttribute(tr ? k_scatter<F64, true> : k_scatter<F64, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)std::max({scatter_smem_bytes(kMaxK),
+                                           scatter_unstable_smem_bytes(kMaxK),
+                                           win_scratch_bytes(kMaxK)})));
+  }
 
   done = true;
 }
@@ -372,7 +392,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     Fill* fills = at<Fill>(fixed, FL.fills[cur]);
 
     // per-level metadata, sized by this level's actual counts
-    const MetaLayout ML = meta_layout(nseg, nchunk, nsample, k);
+    const MetaLayout ML = meta_layout(nseg, nchunk, nsample, k, p.tree);
     void* meta = d_meta_in;
     bool clear_status = false;
     if (meta_cache) {
@@ -395,6 +415,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     uint64_t* seg_dst = at<uint64_t>(meta, ML.seg_dst);
     uint32_t* seg_tot = at<uint32_t>(meta, ML.seg_tot);
     uint32_t* chunk_pre = at<uint32_t>(meta, ML.chunk_pre);
+    uint64_t* tree = p.tree ? at<uint64_t>(meta, ML.tree) : nullptr;
 
     ck(cudaMemsetAsync(nctr, 0, sizeof(LevelCounters), st));
     ck(cudaMemsetAsync(at<uint32_t>(meta, ML.seg_done), 0, (size_t)nseg * 4, st));
@@ -404,16 +425,16 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
       uint32_t* redo = at<uint32_t>(meta, ML.seg_term);  // scratch until K2 writes seg_term
       if (max_S <= (uint32_t)kFMMax)
         k_fit_small<F64, kFSThreads, kFMItems><<<nseg, kFSThreads, kFMSmem, st>>>(
-            src, segs, seed, level, k, trace ? samples : nullptr, models, redo);
+            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree);
       else if (max_S <= (uint32_t)kFSMax)
         k_fit_small<F64, kFSThreads, kFSItems><<<nseg, kFSThreads, kFSSmem, st>>>(
-            src, segs, seed, level, k, trace ? samples : nullptr, models, redo);
+            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree);
       else
         k_fit_small<F64, kFLThreads, kFLItems><<<nseg, kFLThreads, kFLSmem, st>>>(
-            src, segs, seed, level, k, trace ? samples : nullptr, models, redo);
+            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree);
       ck_launch();
       k_gather_fit<F64><<<nseg, kFitThreads, fit_smem(cap), st>>>(
-          src, segs, seed, level, k, cap, trace ? samples : nullptr, models, nullptr, redo);
+          src, segs, seed, level, k, cap, trace ? samples : nullptr, models, nullptr, redo, tree);
       ck_launch();
     }
     LevelArgs la{};
@@ -441,12 +462,11 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     la.wins_big = wbig; la.cap_wbig = p.cap_wbig;
     {
       IPLS_PROF("classify_scan", 8.0 * level_keys);
-      k_classify_scan<F64><<<nchunk, kCThreads, classify_smem(k), st>>>(la);
-      ck_launch();
+      launch_classify<F64>(nchunk, st, la, p.tree);
     }
     {
       IPLS_PROF("scatter", 16.0 * level_keys);
-      launch_scatter<F64>(nchunk, st, la, keys, scr);
+      launch_scatter<F64>(nchunk, st, la, keys, scr, p.tree);
     }
 
     if (trace) {
@@ -475,7 +495,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
         r.requeued = 0;
         for (uint32_t b = 0; b < r.k_eff; ++b) {
           c[b] = ht[(size_t)s * k + b];
-          if (hm[s].kind == kModelLinear && c[b] == hs[s].m) r.requeued = 1;
+          if (hm[s].kind != kModelEq3 && c[b] == hs[s].m) r.requeued = 1;
         }
         std::vector<uint64_t> smp(hsmp.begin() + hs[s].sample_off,
                                   hsmp.begin() + hs[s].sample_off + hs[s].S);
@@ -526,7 +546,9 @@ ipls_status check_cfg(const ipls_config* cfg, ipls_config* out) {
   ipls_config c = cfg ? *cfg : ipls_default_config();
   if (c.k < 3 || c.k > IPLS_MAX_K) return IPLS_ERR_INVALID_ARGUMENT;
   if (c.base_case < 1 || c.base_case > IPLS_MAX_BASE_CASE) return IPLS_ERR_INVALID_ARGUMENT;
-  if (c.flags != 0) return IPLS_ERR_INVALID_ARGUMENT;
+  if (c.flags & ~IPLS_FLAG_TREE_MODEL) return IPLS_ERR_INVALID_ARGUMENT;
+  if ((c.flags & IPLS_FLAG_TREE_MODEL) && (c.k < 4 || (c.k & (c.k - 1)) != 0))
+    return IPLS_ERR_INVALID_ARGUMENT;  // the splitter tree is a perfect binary tree
   *out = c;
   return IPLS_OK;
 }
@@ -543,7 +565,7 @@ ipls_status sort_impl(void* d_keys, size_t n, ipls_key_type t, const ipls_config
   if (n <= 1) return IPLS_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   try {
-    const Params p = make_params(n, cfg.k, cfg.base_case);
+    const Params p = make_params(n, cfg.k, cfg.base_case, (cfg.flags & IPLS_FLAG_TREE_MODEL) != 0);
     const FixedLayout FL = fixed_layout(p);
     StreamCache& sc = cache_for(stream);
     void* fixed;
@@ -637,7 +659,7 @@ size_t ipls_workspace_bytes(size_t n, ipls_key_type t, const ipls_config* cfg) {
   ipls_config c;
   if (check_cfg(cfg, &c) != IPLS_OK || (t != IPLS_KEY_F64 && t != IPLS_KEY_U64)) return 0;
   if (n <= 1) return 0;
-  const Params p = make_params(n, c.k, c.base_case);
+  const Params p = make_params(n, c.k, c.base_case, (c.flags & IPLS_FLAG_TREE_MODEL) != 0);
   return fixed_layout(p).total + worst_meta_bytes(p);
 }
 
@@ -685,11 +707,13 @@ ipls_status ipls_fit_fmcd(const void* d_sorted_sample, size_t S, ipls_key_type t
     if (t == IPLS_KEY_F64) {
       set_attrs<true>();
       k_gather_fit<true><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, k, cap,
-                                                                nullptr, dmod, smp, nullptr);
+                                                                nullptr, dmod, smp, nullptr,
+                                                                nullptr);
     } else {
       set_attrs<false>();
       k_gather_fit<false><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, k, cap,
-                                                                 nullptr, dmod, smp, nullptr);
+                                                                 nullptr, dmod, smp, nullptr,
+                                                                 nullptr);
     }
     ck_launch();
     ModelDev hm;
@@ -772,7 +796,7 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
     auto body = [&](auto f64tag) {
       constexpr bool F64 = decltype(f64tag)::value;
       set_attrs<F64>();
-      k_classify_scan<F64><<<nchunk, kCThreads, classify_smem(k), st>>>(la);
+      launch_classify<F64>(nchunk, st, la);
       ck_launch();
       launch_scatter<F64>(nchunk, st, la, out, out);
     };

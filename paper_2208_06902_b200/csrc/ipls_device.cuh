@@ -14,6 +14,7 @@ namespace ipls {
 
 constexpr uint32_t kModelLinear = 0;
 constexpr uint32_t kModelEq3 = 1;
+constexpr uint32_t kModelTree = 2;   // splitter tree (IPS4o's classifier)
 constexpr uint32_t kSegForceEq3 = 1u;
 constexpr uint64_t kDstUserBit = 1ull << 63;  // seg_dst encoding: buffer select
 constexpr uint32_t kInhBit = 1u << 31;        // count word: child not homogeneous
@@ -28,10 +29,11 @@ struct SegDesc {            // one partition work item of a level (segment of th
   uint32_t pad;
 };
 
-struct ModelDev {           // fitted model of one segment (Listing 1 outputs or EQ3)
+struct ModelDev {           // fitted model of one segment (Listing 1 outputs, EQ3 or a tree)
   double A, B;
   uint64_t pivot_ok;
   uint32_t kind, D, capped, k_eff;
+  const uint64_t* heap;     // tree: splitters (ordering keys) in heap order, heap[1..k-1]
 };
 
 struct ChunkDesc {          // a run of <= CHUNK keys of one segment, processed by one CTA
@@ -92,18 +94,32 @@ __device__ __forceinline__ uint32_t linear_bucket(double v, double A, double B, 
   return min(__double2uint_rz(y), km1);
 }
 
-// Bucket function with the model kind fixed at compile time (the kind is uniform per chunk).
-template <bool F64, bool EQ3>
+// Bucket function with the model kind (MODE = kModelLinear / kModelEq3 / kModelTree) fixed
+// at compile time (the kind is uniform per chunk).  Tree: the branchless descent
+// j <- 2j + (x > a_j) of P:377-379 over the implicit tree of the k-1 splitters (k a power of
+// two), read through the L1 (8 KB per segment: the upper levels stay resident); ties go left
+// (R23).
+template <bool F64, int MODE>
 struct Bucketer {
   double A, B;
   uint64_t piv;
   uint32_t km1;
+  const uint64_t* heap;
+  int depth;
   __device__ __forceinline__ explicit Bucketer(const ModelDev& md, uint32_t k)
-      : A(md.A), B(md.B), piv(md.pivot_ok), km1(k - 1) {}
+      : A(md.A), B(md.B), piv(md.pivot_ok), km1(k - 1), heap(md.heap), depth(0) {
+    if constexpr (MODE == (int)kModelTree)
+      while ((2u << depth) <= k) ++depth;  // log2 k (k a power of two)
+  }
   __device__ __forceinline__ uint32_t operator()(uint64_t bits) const {
-    if constexpr (EQ3) {
+    if constexpr (MODE == (int)kModelEq3) {
       const uint64_t o = ok_of<F64>(bits);
       return (o < piv) ? 0u : ((o == piv) ? 1u : 2u);
+    } else if constexpr (MODE == (int)kModelTree) {
+      const uint64_t o = ok_of<F64>(bits);
+      uint32_t j = 1;
+      for (int d = 0; d < depth; ++d) j = 2 * j + (o > __ldg(heap + j) ? 1u : 0u);
+      return j - (km1 + 1);
     } else {
       return linear_bucket(value_of<F64>(bits), A, B, km1);
     }

@@ -225,12 +225,27 @@ __device__ bool fmcd_pred(const double* s, uint32_t N, uint32_t D, double u) {
   return __syncthreads_or(fail) == 0;
 }
 
+// Splitter tree (R22): node j (1..k-1, heap order) of the perfect tree of
+// depth log2 k holds the splitter of in-order rank i = (2 p + 1) 2^(L-1-d) (d = depth of j,
+// p = j - 2^d), and splitter i is the order statistic s[floor(i S / k)] of the sorted sample
+// `so` (ordering keys).  One thread per node.
+template <int NT>
+__device__ __forceinline__ void write_tree(const uint64_t* so, uint32_t S, uint32_t k,
+                                           uint64_t* heap) {
+  const int L = 31 - __clz(k);
+  for (uint32_t j = threadIdx.x + 1; j < k; j += NT) {
+    const int d = 31 - __clz(j);
+    const uint32_t i = (2 * (j - (1u << d)) + 1) << (L - 1 - d);
+    heap[j] = so[(uint32_t)(((uint64_t)i * S) >> L)];
+  }
+}
+
 template <bool F64>
 __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
     uint32_t level, uint32_t k, uint32_t cap, uint64_t* __restrict__ samples_out,
     ModelDev* __restrict__ models, const uint64_t* __restrict__ presorted_ok,
-    const uint32_t* __restrict__ redo) {
+    const uint32_t* __restrict__ redo, uint64_t* __restrict__ tree) {
   if (redo && !redo[blockIdx.x]) return;  // fitted by k_fit_small
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* a = reinterpret_cast<uint64_t*>(smraw);   // cap
@@ -278,7 +293,11 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
   ModelDev md{};
   md.k_eff = k;
   bool eq3 = (sg.flags & kSegForceEq3) || S < 4;
-  if (!eq3) {
+  if (!eq3 && tree) {  // splitter-tree model instead of FMCD
+    uint64_t* hp = tree + (size_t)blockIdx.x * kMaxK;
+    write_tree<kFitThreads>(a, S, k, hp);
+    md.kind = kModelTree; md.heap = hp;
+  } else if (!eq3) {
     double* s = reinterpret_cast<double*>(tmp);
     for (uint32_t i = threadIdx.x; i < S; i += kFitThreads) s[i] = value_of<F64>(bits_of_ok<F64>(a[i]));
     __syncthreads();
@@ -354,7 +373,7 @@ template <bool F64, int NT, int IT>
 __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
     const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
     uint32_t level, uint32_t k, uint64_t* __restrict__ samples_out, ModelDev* __restrict__ models,
-    uint32_t* __restrict__ redo) {
+    uint32_t* __restrict__ redo, uint64_t* __restrict__ tree) {
   constexpr int NW = NT / 32, SMAX = NT * IT;
   static_assert(NT >= 256 && IT % 4 == 0, "256 coarse bins, uint4 fine-bin scan");
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -589,7 +608,11 @@ __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
   ModelDev md{};
   md.k_eff = k;
   bool eq3 = (sg.flags & kSegForceEq3) || S < 4;
-  if (!eq3) {
+  if (!eq3 && tree) {  // splitter-tree model instead of FMCD
+    uint64_t* hp = tree + (size_t)blockIdx.x * kMaxK;
+    write_tree<NT>(B, S, k, hp);
+    md.kind = kModelTree; md.heap = hp;
+  } else if (!eq3) {
     double* s = reinterpret_cast<double*>(B);
     for (uint32_t i = threadIdx.x; i < S; i += NT) s[i] = value_of<F64>(bits_of_ok<F64>(B[i]));
     __syncthreads();
@@ -905,7 +928,7 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
   int st = 0;
 #pragma unroll
   for (int q = 0; q < BPT; ++q)
-    if (md.kind == kModelLinear && bb[q] < k && tot[q] == sg.m) st = 1;
+    if (md.kind != kModelEq3 && bb[q] < k && tot[q] == sg.m) st = 1;  // R10, R24
   const bool stuck = __syncthreads_or(st) != 0;
   const uint32_t dstbuf = (a.level + 1) & 1;  // 1 = scratch, 0 = user array
   uint32_t cls[BPT];
@@ -1008,10 +1031,10 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
 // Per key: model evaluation (2 RN ops + saturating convert) and one smem atomicAdd into the
 // chunk histogram (+ the NaN test at level 0).  The next tile is loaded while this one is
 // classified.
-template <bool F64, bool EQ3, bool NANCHK, bool IDS>
+template <bool F64, int MODE, bool NANCHK, bool IDS>
 __device__ void classify_tiles(const LevelArgs& a, const ChunkDesc& ch, const ModelDev& md,
                                uint32_t* hist, int& nan_seen) {
-  const Bucketer<F64, EQ3> bucket(md, a.k);
+  const Bucketer<F64, MODE> bucket(md, a.k);
   const uint64_t* p = a.src + ch.start;
   uint64_t cur[kCItems], nxt[kCItems];
 #pragma unroll
@@ -1044,19 +1067,22 @@ __device__ void classify_tiles(const LevelArgs& a, const ChunkDesc& ch, const Mo
   nan_seen = nan ? 1 : 0;
 }
 
-template <bool F64, bool EQ3>
+template <bool F64, int MODE>
 __device__ __forceinline__ void classify_dispatch(const LevelArgs& a, const ChunkDesc& ch,
                                                   const ModelDev& md, uint32_t* hist,
                                                   int& nan_seen) {
   if (a.ids)
-    classify_tiles<F64, EQ3, false, true>(a, ch, md, hist, nan_seen);
+    classify_tiles<F64, MODE, false, true>(a, ch, md, hist, nan_seen);
   else if (F64 && a.check_nan)
-    classify_tiles<F64, EQ3, F64, false>(a, ch, md, hist, nan_seen);
+    classify_tiles<F64, MODE, F64, false>(a, ch, md, hist, nan_seen);
   else
-    classify_tiles<F64, EQ3, false, false>(a, ch, md, hist, nan_seen);
+    classify_tiles<F64, MODE, false, false>(a, ch, md, hist, nan_seen);
 }
 
-template <bool F64>
+// TREE selects the kernel instantiation of the splitter-tree model (IPLS_FLAG_TREE_MODEL):
+// its segments are TREE or EQ3, the default instantiation's LINEAR or EQ3, so each kernel
+// carries two bucket functions only.
+template <bool F64, bool TREE>
 __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const uint32_t k = a.k;
@@ -1072,9 +1098,9 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
   const ModelDev md = a.models[ch.seg];
   int nan_seen = 0;
   if (md.kind == kModelEq3)
-    classify_dispatch<F64, true>(a, ch, md, hist, nan_seen);
+    classify_dispatch<F64, kModelEq3>(a, ch, md, hist, nan_seen);
   else
-    classify_dispatch<F64, false>(a, ch, md, hist, nan_seen);
+    classify_dispatch<F64, TREE ? kModelTree : kModelLinear>(a, ch, md, hist, nan_seen);
   if (a.check_nan) {
     if (__syncthreads_or(nan_seen) && threadIdx.x == 0) atomicOr(a.err, kErrNan);
   } else {
@@ -1150,7 +1176,7 @@ __host__ __device__ constexpr size_t scatter_smem_bytes(uint32_t k) {
          (size_t)kSPairs4 * k * 4 + (size_t)(k + 1) * 4 + (size_t)k + 16;
 }
 
-template <bool F64, bool EQ3>
+template <bool F64, int MODE>
 __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_user,
                               uint64_t* __restrict__ dst_scr, uint32_t c, const ChunkDesc& ch,
                               const ModelDev& md, unsigned char* smraw) {
@@ -1165,7 +1191,7 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
   uint32_t* toff = sbi + kSTile4;                                // k + 1
   uint8_t* cflag = reinterpret_cast<uint8_t*>(toff + k + 1);     // k
   __shared__ uint32_t s_warp[40];
-  const Bucketer<F64, EQ3> bucket(md, k);
+  const Bucketer<F64, MODE> bucket(md, k);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   for (uint32_t b = threadIdx.x; b < k; b += NT) {
     const uint64_t d = a.seg_dst[(size_t)ch.seg * k + b] + a.chunk_pre[(size_t)c * k + b];
@@ -1345,7 +1371,7 @@ __host__ __device__ constexpr size_t scatter_unstable_smem_bytes(uint32_t k) {
   return (size_t)kUTile * 8 + (size_t)k * 8 * 2 + (size_t)k * 4 * 2;
 }
 
-template <bool F64, bool EQ3>
+template <bool F64, int MODE>
 __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict__ dst_user,
                                        uint64_t* __restrict__ dst_scr, uint32_t c,
                                        const ChunkDesc& ch, const ModelDev& md,
@@ -1358,7 +1384,7 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
   uint32_t* cnt = reinterpret_cast<uint32_t*>(adj + k);           // k
   uint32_t* cur = cnt + k;                                        // k
   __shared__ uint32_t s_warp[40];
-  const Bucketer<F64, EQ3> bucket(md, k);
+  const Bucketer<F64, MODE> bucket(md, k);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   for (uint32_t b = threadIdx.x; b < k; b += NT) {
     const uint64_t d = a.seg_dst[(size_t)ch.seg * k + b] + a.chunk_pre[(size_t)c * k + b];
@@ -1445,7 +1471,7 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
   }
 }
 
-template <bool F64>
+template <bool F64, bool TREE>
 __global__ __launch_bounds__(kSThreads4, 1) void k_scatter(LevelArgs a, uint64_t* __restrict__ dst_user,
                                                            uint64_t* __restrict__ dst_scr) {
   if (*((volatile const uint32_t*)a.err) & kErrNan) return;
@@ -1456,15 +1482,16 @@ __global__ __launch_bounds__(kSThreads4, 1) void k_scatter(LevelArgs a, uint64_t
   const ChunkDesc ch = a.chunks[c];
   const ModelDev md = a.models[ch.seg];
   const bool terminal = !a.single_offsets && a.seg_term[ch.seg];
+  constexpr int kMain = TREE ? (int)kModelTree : (int)kModelLinear;
   if (terminal) {
     if (md.kind == kModelEq3)
-      scatter_chunk_unstable<F64, true>(a, dst_user, dst_scr, c, ch, md, smraw);
+      scatter_chunk_unstable<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw);
     else
-      scatter_chunk_unstable<F64, false>(a, dst_user, dst_scr, c, ch, md, smraw);
+      scatter_chunk_unstable<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
   } else if (md.kind == kModelEq3) {
-    scatter_chunk<F64, true>(a, dst_user, dst_scr, c, ch, md, smraw);
+    scatter_chunk<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw);
   } else {
-    scatter_chunk<F64, false>(a, dst_user, dst_scr, c, ch, md, smraw);
+    scatter_chunk<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
   }
   if (a.single_offsets) return;  // ipls_partition_level: no next level
   const SegDesc sg = a.segs[ch.seg];

@@ -215,6 +215,49 @@ def test_paper_workloads_parity(ipls, name, n, k):
     compare_traces(gtr, ores)
 
 
+TREE_KINDS = ["uniform", "normal", "lognormal", "few_distinct", "two_values", "signed_zeros",
+              "infs", "u64_above_2_53", "root_dups_u64", "mixture"]
+
+
+@pytest.mark.parametrize("kind", TREE_KINDS)
+@pytest.mark.parametrize("n,k,B", [(5000, 16, 64), (70_001, 256, 4096), (300_000, 1024, 4096)])
+def test_tree_model_parity(ipls, kind, n, k, B):
+    """Splitter-tree model (R22-R24): samples, tree kind, per-segment counts,
+    every level's layout and the final array, bit-exact against the oracle's tree model."""
+    rng = np.random.default_rng(n + k + len(kind))
+    a = datagen.fuzz_array(rng, n, kind)
+    want = a.copy()
+    ores = oracle.sort(want, k=k, base_case=B, trace=True, snapshots=True,
+                       model=oracle.MODEL_TREE)
+    t = dev(a)
+    gtr = ipls.sort_trace(t, k=k, base_case=B, key_type=kt_of(a),
+                          snapshot_levels=max(1, ores.levels), model=ipls.MODEL_TREE)
+    assert host(t, a.dtype).tobytes() == want.tobytes()
+    compare_traces(gtr, ores)
+    assert any(r.kind == ipls.MODEL_TREE for r in gtr.records) or kind in ("few_distinct",
+                                                                           "two_values")
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+def test_tree_model_configs_scaled(ipls, name):
+    a = datagen.generate(name, 2_000_000)
+    cfg = datagen.CONFIGS[name]
+    want = a.copy()
+    ores = oracle.sort(want, k=cfg.k, base_case=cfg.base_case, trace=True,
+                       model=oracle.MODEL_TREE)
+    t = dev(a)
+    gtr = ipls.sort_trace(t, k=cfg.k, base_case=cfg.base_case, key_type=kt_of(a),
+                          model=ipls.MODEL_TREE)
+    assert host(t, a.dtype).tobytes() == want.tobytes()
+    compare_traces(gtr, ores)
+
+
+def test_tree_model_rejects_k_not_power_of_two(ipls):
+    t = dev(np.random.default_rng(0).random(10000))
+    with pytest.raises(ipls.IPLSError):
+        ipls.sort(t, k=1000, model=ipls.MODEL_TREE)
+
+
 def test_worked_example_sort(ipls, golden):
     x = np.array([float(v) for v in golden("worked_example.txt")["input"][0]])
     t = dev(x)
