@@ -34,6 +34,7 @@ struct ModelDev {           // fitted model of one segment (Listing 1 outputs, E
   uint64_t pivot_ok;
   uint32_t kind, D, capped, k_eff;
   const uint64_t* heap;     // tree: splitters (ordering keys) in heap order, heap[1..k-1]
+  const uint64_t* top;      // tree, set per CTA: smem copy of heap[0..256) (the top 8 levels)
 };
 
 struct ChunkDesc {          // a run of <= CHUNK keys of one segment, processed by one CTA
@@ -97,17 +98,18 @@ __device__ __forceinline__ uint32_t linear_bucket(double v, double A, double B, 
 // Bucket function with the model kind (MODE = kModelLinear / kModelEq3 / kModelTree) fixed
 // at compile time (the kind is uniform per chunk).  Tree: the branchless descent
 // j <- 2j + (x > a_j) of P:377-379 over the implicit tree of the k-1 splitters (k a power of
-// two), read through the L1 (8 KB per segment: the upper levels stay resident); ties go left
-// (R23).
+// two); the top 8 levels come from the CTA's smem copy, deeper levels through the L1; ties go
+// left (R23).
 template <bool F64, int MODE>
 struct Bucketer {
   double A, B;
   uint64_t piv;
   uint32_t km1;
   const uint64_t* heap;
+  const uint64_t* top;
   int depth;
   __device__ __forceinline__ explicit Bucketer(const ModelDev& md, uint32_t k)
-      : A(md.A), B(md.B), piv(md.pivot_ok), km1(k - 1), heap(md.heap), depth(0) {
+      : A(md.A), B(md.B), piv(md.pivot_ok), km1(k - 1), heap(md.heap), top(md.top), depth(0) {
     if constexpr (MODE == (int)kModelTree)
       while ((2u << depth) <= k) ++depth;  // log2 k (k a power of two)
   }
@@ -118,7 +120,9 @@ struct Bucketer {
     } else if constexpr (MODE == (int)kModelTree) {
       const uint64_t o = ok_of<F64>(bits);
       uint32_t j = 1;
-      for (int d = 0; d < depth; ++d) j = 2 * j + (o > __ldg(heap + j) ? 1u : 0u);
+      const int dt = depth < 8 ? depth : 8;
+      for (int d = 0; d < dt; ++d) j = 2 * j + (o > top[j] ? 1u : 0u);
+      for (int d = dt; d < depth; ++d) j = 2 * j + (o > __ldg(heap + j) ? 1u : 0u);
       return j - (km1 + 1);
     } else {
       return linear_bucket(value_of<F64>(bits), A, B, km1);

@@ -1095,7 +1095,14 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
   const uint32_t c = s_c;
   const ChunkDesc ch = a.chunks[c];
   const SegDesc sg = a.segs[ch.seg];
-  const ModelDev md = a.models[ch.seg];
+  ModelDev md = a.models[ch.seg];
+  if constexpr (TREE) {  // top 8 levels of the splitter heap into smem
+    __shared__ uint64_t s_top[256];
+    if (md.kind == kModelTree)
+      for (uint32_t j = threadIdx.x; j < min(k, 256u); j += kCThreads) s_top[j] = md.heap[j];
+    md.top = s_top;
+    __syncthreads();
+  }
   int nan_seen = 0;
   if (md.kind == kModelEq3)
     classify_dispatch<F64, kModelEq3>(a, ch, md, hist, nan_seen);
@@ -1368,7 +1375,7 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
 constexpr int kURounds = IPLS_UROUNDS;             // keys per thread per tile
 constexpr int kUTile = kSThreads4 * kURounds;      // 16384
 __host__ __device__ constexpr size_t scatter_unstable_smem_bytes(uint32_t k) {
-  return (size_t)kUTile * 8 + (size_t)k * 8 * 2 + (size_t)k * 4 * 2;
+  return (size_t)kUTile * 8 + (size_t)k * 8 * 2 + (size_t)k * 4 * 2 + (size_t)kUTile * 2;
 }
 
 template <bool F64, int MODE>
@@ -1383,6 +1390,7 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
   uint64_t* adj = runa + k;                                       // k
   uint32_t* cnt = reinterpret_cast<uint32_t*>(adj + k);           // k
   uint32_t* cur = cnt + k;                                        // k
+  uint16_t* sbk = reinterpret_cast<uint16_t*>(cur + k);           // kUTile (tree only)
   __shared__ uint32_t s_warp[40];
   const Bucketer<F64, MODE> bucket(md, k);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
@@ -1450,7 +1458,9 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
     for (int r = 0; r < kURounds; ++r) {
       const uint32_t bb = (bk[r >> 1] >> (16 * (r & 1))) & 0xffffu;
       if (bb != 0xffffu) {
-        stage[atomicAdd(&cur[bb], 1u)] = key[r];
+        const uint32_t pos = atomicAdd(&cur[bb], 1u);
+        stage[pos] = key[r];
+        if constexpr (MODE == (int)kModelTree) sbk[pos] = (uint16_t)bb;
       }
     }
 #pragma unroll
@@ -1464,7 +1474,10 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
     // than a random 2-byte smem store in the placement and a load here
     for (uint32_t q = threadIdx.x; q < tl; q += NT) {
       const uint64_t x = stage[q];
-      st_evict_last(reinterpret_cast<uint64_t*>(adj[bucket(x)]) + q, x);
+      uint32_t b;
+      if constexpr (MODE == (int)kModelTree) b = sbk[q];  // a tree descent costs more
+      else b = bucket(x);
+      st_evict_last(reinterpret_cast<uint64_t*>(adj[b]) + q, x);
     }
     __syncthreads();
     SC_TICK(7);
@@ -1480,7 +1493,14 @@ __global__ __launch_bounds__(kSThreads4, 1) void k_scatter(LevelArgs a, uint64_t
   __shared__ uint32_t s_last;
   const uint32_t c = blockIdx.x;
   const ChunkDesc ch = a.chunks[c];
-  const ModelDev md = a.models[ch.seg];
+  ModelDev md = a.models[ch.seg];
+  if constexpr (TREE) {  // top 8 levels of the splitter heap into smem
+    __shared__ uint64_t s_top[256];
+    if (md.kind == kModelTree)
+      for (uint32_t j = threadIdx.x; j < min(a.k, 256u); j += kSThreads4) s_top[j] = md.heap[j];
+    md.top = s_top;
+    __syncthreads();
+  }
   const bool terminal = !a.single_offsets && a.seg_term[ch.seg];
   constexpr int kMain = TREE ? (int)kModelTree : (int)kModelLinear;
   if (terminal) {

@@ -8,7 +8,9 @@ torch.sort of the input in ordering-key order (sorted, same multiset).  Inputs: 
 workloads from datagen.paper_workload (numpy PCG64(7)); the sweep draws Normal(0,1) on the GPU
 with torch.Generator(cuda).manual_seed(11) (1e9 keys would take a minute on the host).
 
-usage: python tools/sweep.py [--part workloads|sizes|all] [--out FILE]
+usage: python tools/sweep.py [--part workloads|sizes|models|all] [--out FILE]
+  models: C1-C5 with the FMCD linear model (IPLS) and with the splitter tree (IPS4o's
+  classifier, IPLS_FLAG_TREE_MODEL) on the same framework.
 """
 import argparse, json, math, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -29,7 +31,7 @@ def signed_order(t, f64):
     return t ^ SIGN
 
 
-def run_case(x, f64, reps, warm=3):
+def run_case(x, f64, reps, warm=3, k=K, base_case=B, model=ipls.MODEL_LINEAR):
     work = torch.empty_like(x)
     kt = ipls.KEY_F64 if f64 else ipls.KEY_U64
     times = []
@@ -38,7 +40,7 @@ def run_case(x, f64, reps, warm=3):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        ipls.sort(work, k=K, base_case=B, key_type=kt)
+        ipls.sort(work, k=k, base_case=base_case, key_type=kt, model=model)
         e1.record()
         torch.cuda.synchronize()
         if i >= warm:
@@ -50,7 +52,7 @@ def run_case(x, f64, reps, warm=3):
     del ref, got, work
     n = x.numel()
     ms = statistics.median(times)
-    lstar = max(1, math.ceil(math.log(math.ceil(n / B), K))) if n > B else 0
+    lstar = max(1, math.ceil(math.log(math.ceil(n / base_case), k))) if n > base_case else 0
     model = 16 * n * (lstar + 1)
     return {"n": n, "ms": round(ms, 4), "keys_per_s": n / (ms / 1e3),
             "frac_of_8TBps": round(model / 8e12 / (ms / 1e3), 4), "L*": lstar,
@@ -73,6 +75,18 @@ def main():
             r["desc"] = desc
             res["workloads"][name] = r
             print(name, json.dumps(r), flush=True)
+            del x
+    if args.part in ("models", "all"):
+        res["models"] = {}
+        for name in ["C1", "C2", "C3", "C4", "C5"]:
+            cfg = datagen.CONFIGS[name]
+            a = datagen.generate(name)
+            x = torch.from_numpy(a.view(np.int64)).cuda()
+            for model, mname in [(ipls.MODEL_LINEAR, "fmcd"), (ipls.MODEL_TREE, "tree")]:
+                r = run_case(x, a.dtype == np.float64, reps=10, k=cfg.k, base_case=cfg.base_case,
+                             model=model)
+                res["models"][f"{name}/{mname}"] = r
+                print(name, mname, json.dumps(r), flush=True)
             del x
     if args.part in ("sizes", "all"):
         res["normal_sizes"] = []

@@ -28,7 +28,8 @@ for name in names:
             ipls.profile_reset(); ipls.profile_enable(True)
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        ipls.sort(t, k=cfg.k, base_case=cfg.base_case, key_type=kt)
+        ipls.sort(t, k=cfg.k, base_case=cfg.base_case, key_type=kt,
+                  model=int(os.environ.get("MODEL", "0")))
         e1.record(); torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
     ipls.profile_enable(False)
