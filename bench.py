@@ -221,6 +221,9 @@ def main():
                     help="keys of the workload the CPU oracle sorts for cpu_baseline")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--model", default="fmcd", choices=["fmcd", "tree"],
+                    help="partition model: fmcd (IPLS, the default and the headline) or tree "
+                         "(IPS4o's splitter tree on the same kernels, SURVEY NEXT #2)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (default: the "
                          "committed profiles/r01_traffic.json capture)")
@@ -245,11 +248,12 @@ def main():
     work = torch.empty_like(pristine)
     st = torch.cuda.current_stream()
 
+    model = ipls.MODEL_TREE if args.model == "tree" else ipls.MODEL_LINEAR
     def one(timed_events=None):
         work.copy_(pristine)
         if timed_events is not None:
             timed_events[0].record(st)
-        ipls.sort(work, k=cfg.k, base_case=cfg.base_case, key_type=kt)
+        ipls.sort(work, k=cfg.k, base_case=cfg.base_case, key_type=kt, model=model)
         if timed_events is not None:
             timed_events[1].record(st)
 
@@ -329,7 +333,7 @@ def main():
         barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ipls.sort_host_ptr(hbuf.data_ptr(), n, kt, k=cfg.k, base_case=cfg.base_case)
+        ipls.sort_host_ptr(hbuf.data_ptr(), n, kt, k=cfg.k, base_case=cfg.base_case, model=model)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if i > 0:
@@ -352,6 +356,7 @@ def main():
             "dtype": "f64" if kt == ipls.KEY_F64 else "u64", "data": "synthetic",
             "config": {
                 "workload": f"{args.config}: {cfg.desc}, n={n}, k={cfg.k}, base_case={cfg.base_case}",
+                "model": args.model,
                 "parallelism": "replicas" if world > 1 else "single-gpu",
                 "l2": "input 0.8 GB > L2 126 MB; pristine copy restored (D2D) before every step",
                 "timing": "CUDA events around each ipls_sort_ex call on its stream; mean over steps; max over ranks",

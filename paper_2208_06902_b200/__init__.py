@@ -203,18 +203,18 @@ def workspace_bytes(n: int, key_type: int = KEY_F64, k: int = 256, base_case: in
 
 
 def sort_host(keys: np.ndarray, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SEED,
-              stream=None) -> None:
+              stream=None, model: int = MODEL_LINEAR) -> None:
     """Sort a host numpy array (float64/uint64; ideally pinned memory) through the library."""
     if not keys.flags.c_contiguous or keys.dtype.itemsize != 8:
         raise ValueError("keys must be a contiguous 8-byte numpy array")
     kt = KEY_F64 if keys.dtype == np.float64 else KEY_U64
-    c = _cfg(k, base_case, seed)
+    c = _cfg(k, base_case, seed, model)
     _check(lib().ipls_sort_host(keys.ctypes.data, keys.size, kt, ctypes.byref(c), _stream(stream)))
 
 
 def sort_host_ptr(ptr: int, n: int, key_type: int, k: int = 256, base_case: int = 4096,
-                  seed: int = DEFAULT_SEED, stream=None) -> None:
-    c = _cfg(k, base_case, seed)
+                  seed: int = DEFAULT_SEED, stream=None, model: int = MODEL_LINEAR) -> None:
+    c = _cfg(k, base_case, seed, model)
     _check(lib().ipls_sort_host(ptr, n, key_type, ctypes.byref(c), _stream(stream)))
 
 
