@@ -82,9 +82,6 @@ __device__ __forceinline__ double value_of(uint64_t bits) {
   if constexpr (F64) return __longlong_as_double((long long)bits);
   else return __ull2double_rn(bits);
 }
-__device__ __forceinline__ bool is_nan_bits(uint64_t bits) {
-  return ((bits >> 52) & 0x7ff) == 0x7ff && (bits & 0xfffffffffffffull) != 0;
-}
 
 // P:394-402 with R7: 0 if !(y >= 0); k-1 if y >= k; floor(y) otherwise, y = RN(RN(A*v) + B).
 // cvt.rzi.u32.f64 (__double2uint_rz) truncates toward zero and saturates: y < 0 (also -inf,
