@@ -93,3 +93,21 @@ def test_c1_full_size_equals_numpy():
     want = np.sort(a)
     assert oracle.sort(a, k=256, base_case=4096).status == 0
     assert a.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("name", list(datagen.PAPER_WORKLOADS))
+def test_paper_workloads_match_numpy(name):
+    """The paper's nine synthetic workloads through the oracle, k = 1024 and 256."""
+    for n, k in [(60_000, 1024), (30_000, 256)]:
+        a = datagen.paper_workload(name, n)
+        want = ref_sorted(a)
+        assert oracle.sort(a, k=k, base_case=4096).status == 0
+        assert a.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("kind", datagen.STRESS_KINDS)
+def test_stress_arrays_match_numpy(kind):
+    a = datagen.stress_array(np.random.default_rng(3), 50_000, kind)
+    want = ref_sorted(a)
+    assert oracle.sort(a, k=256, base_case=4096).status == 0
+    assert a.tobytes() == want.tobytes()
