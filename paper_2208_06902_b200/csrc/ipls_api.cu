@@ -115,12 +115,15 @@ struct Params {
 };
 
 #ifndef IPLS_CHUNK_CAP
-#define IPLS_CHUNK_CAP 65536
+#define IPLS_CHUNK_CAP 98304
 #endif
 uint32_t pick_chunk_keys(uint64_t n) {
-  // ~8 chunks per SM at level 0 (148 SMs), whole tiles, 4096..65536 keys.
+  // ~8 chunks per SM at level 0 (148 SMs), 4096..98304 keys; from 16384 keys up a multiple of
+  // the terminal scatter's 16384-key tile.  Larger chunks amortise each chunk's k-wide
+  // lookback, histogram and run setup (98304 keys: C2 -1.2 %, C5 -1.2 % against 65536).
   uint64_t c = n / (148 * 8);
-  c = (c + kCTile - 1) / kCTile * kCTile;
+  if (c >= 16384) c = (c + 16383) / 16384 * 16384;
+  else c = (c + kCTile - 1) / kCTile * kCTile;
   if (c < (uint64_t)kCTile) c = kCTile;
   if (c > IPLS_CHUNK_CAP) c = IPLS_CHUNK_CAP;
   return (uint32_t)c;
