@@ -1748,24 +1748,24 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
     if (s0 + 1 < s1) {
       uint64_t* q = B + s0;  // q[1] is the key being inserted
       uint64_t prev = q[0], pp = 0ull, nx = q[1];
+#pragma unroll 2
       for (uint32_t i = s0 + 1; i < s1; ++i, ++q) {
         const uint64_t x = nx;
-        nx = (i + 1 < s1) ? q[2] : 0ull;  // never written while x is inserted
-        if (x < prev) {
+        nx = q[2];  // never written while x is inserted (may read past the piece: B has
+                    // room, fh follows it)
+        const bool lt = x < prev;
+        const uint64_t m = max(pp, x);
+        if (lt) {
           q[1] = prev;
-          if (x >= pp) {
-            q[0] = x;
-            pp = x;
-          } else {  // rare: x belongs below pp
-            q[0] = pp;
-            uint64_t* r = q - 1;
-            while (r > B + s0 && r[-1] > x) { r[0] = r[-1]; --r; }
-            r[0] = x;
-          }
-        } else {
-          pp = prev;
-          prev = x;
+          q[0] = m;
         }
+        if (lt && x < pp) {  // rare: x belongs below pp (q[0] = pp already)
+          uint64_t* r = q - 1;
+          while (r > B + s0 && r[-1] > x) { r[0] = r[-1]; --r; }
+          r[0] = x;
+        }
+        pp = lt ? m : prev;
+        prev = lt ? prev : x;
       }
     }
     if (!msk) break;
