@@ -35,15 +35,23 @@ def digests(records):
 
 
 def main():
-    names = sys.argv[1:] or list(datagen.CONFIGS)
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle_digests.txt")
-    lines = ["# Written by tests/golden/make_oracle_digests.py (oracle/ only; seed 0x49504C53).",
+    # usage: make_oracle_digests.py [--tree] [cfg ...]; --tree: the splitter-tree model
+    # (IPLS_FLAG_TREE_MODEL, R22-R24) into oracle_digests_tree.txt
+    args = sys.argv[1:]
+    tree = "--tree" in args
+    args = [x for x in args if x != "--tree"]
+    names = args or list(datagen.CONFIGS)
+    fname = "oracle_digests_tree.txt" if tree else "oracle_digests.txt"
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), fname)
+    lines = [f"# Written by tests/golden/make_oracle_digests.py{' --tree' if tree else ''} "
+             "(oracle/ only; seed 0x49504C53).",
              "# LEVEL cfg level n_records records_sha counts_sha samples_sha",
              "# FINAL cfg levels final_sha256"]
     for name in names:
         cfg = datagen.CONFIGS[name]
         a = datagen.generate(name)
-        r = oracle.sort(a, k=cfg.k, base_case=cfg.base_case, trace=True)
+        r = oracle.sort(a, k=cfg.k, base_case=cfg.base_case, trace=True,
+                        model=oracle.MODEL_TREE if tree else oracle.MODEL_LINEAR)
         assert r.status == 0
         for lv, nrec, d1, d2, d3 in digests(r.records):
             lines.append(f"LEVEL {name} {lv} {nrec} {d1} {d2} {d3}")

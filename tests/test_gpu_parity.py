@@ -281,9 +281,9 @@ def test_configs_scaled_full_trace(ipls, name, n):
     compare_traces(gtr, ores)
 
 
-def load_oracle_digests():
+def load_oracle_digests(fname="oracle_digests.txt"):
     lv, fin = {}, {}
-    with open(os.path.join(GOLD, "oracle_digests.txt")) as f:
+    with open(os.path.join(GOLD, fname)) as f:
         for line in f:
             tok = line.split()
             if not tok or tok[0].startswith("#"):
@@ -332,6 +332,22 @@ def test_configs_full_size_vs_oracle_digests(ipls, name):
     t2 = dev(b)
     ipls.sort(t2, k=cfg.k, base_case=cfg.base_case, key_type=kt_of(b))
     assert torch.equal(t, t2)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_tree_configs_full_size_vs_oracle_digests(ipls, name):
+    """Splitter-tree model (NEXT #2) at full BASELINE sizes against oracle-written digests
+    (tests/golden/oracle_digests_tree.txt)."""
+    lvd, fin = load_oracle_digests("oracle_digests_tree.txt")
+    cfg = datagen.CONFIGS[name]
+    a = datagen.generate(name)
+    t = dev(a)
+    del a
+    gtr = ipls.sort_trace(t, k=cfg.k, base_case=cfg.base_case,
+                          key_type=kt_of(datagen.generate(name, 1)), model=ipls.MODEL_TREE)
+    assert gpu_digests(gtr.records) == lvd[name]
+    assert gtr.levels == fin[name][0]
+    assert hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest() == fin[name][1]
 
 
 def test_nan_rejected_unmodified(ipls):
