@@ -350,6 +350,37 @@ def test_tree_configs_full_size_vs_oracle_digests(ipls, name):
     assert hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest() == fin[name][1]
 
 
+def _mix_sum(t, step=1 << 28):
+    """Order-independent multiset digest: wrapping sum of a SplitMix64-style mix of every key
+    (int64 arithmetic on the GPU, in slices to bound the temporaries)."""
+    acc = 0
+    for i in range(0, t.numel(), step):
+        z = t[i:i + step] * -7046029254386353131  # 0x9E3779B97F4A7C15
+        z = (z ^ (z >> 30)) * -4658895280553007687  # 0xBF58476D1CE4E5B9
+        z = (z ^ (z >> 27)) * -7723592293110705685  # 0x94D049BB133111EB
+        acc = (acc + int((z ^ (z >> 31)).sum())) & 0xFFFFFFFFFFFFFFFF
+    return acc
+
+
+def test_api_maximum_size(ipls):
+    """n = 2^32 - 1 keys (34 GB, the ABI's limit, odd): sorted, same multiset (the oracle
+    cannot run at this size; the final array is defined by sortedness + multiset)."""
+    n = 2**32 - 1
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    x = torch.randn(n, dtype=torch.float64, device="cuda", generator=g).view(torch.int64)
+    before = _mix_sum(x)
+    ipls.sort(x, k=1024, base_case=4096, key_type=ipls.KEY_F64)
+    f = x.view(torch.float64)
+    step = 1 << 28
+    for i in range(0, n - 1, step):  # sorted, checked in overlapping slices
+        s = f[i:min(i + step + 1, n)]
+        assert bool((s[1:] >= s[:-1]).all())
+    assert _mix_sum(x) == before
+    del x, f
+    torch.cuda.empty_cache()
+
+
 def test_nan_rejected_unmodified(ipls):
     rng = np.random.default_rng(0)
     for n in (10, 5000, 300_000):
