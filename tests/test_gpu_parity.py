@@ -258,6 +258,23 @@ def test_tree_model_rejects_k_not_power_of_two(ipls):
         ipls.sort(t, k=1000, model=ipls.MODEL_TREE)
 
 
+@pytest.mark.parametrize("k,B,n", [(3, 1, 3000), (5, 17, 20_000), (7, 255, 100_000),
+                                   (100, 4096, 250_000), (1000, 1000, 400_001),
+                                   (513, 257, 150_000), (1023, 4096, 1_500_000)])
+@pytest.mark.parametrize("kind", ["normal", "lognormal", "few_distinct", "u64_big"])
+def test_sort_parity_odd_k_and_base(ipls, k, B, n, kind):
+    """Fan-outs and base-case thresholds other than the configs' (k odd or not a power of two,
+    B from 1 to 4096): full trace and final array against the oracle."""
+    rng = np.random.default_rng(k * 7 + B + len(kind))
+    a = datagen.fuzz_array(rng, n, kind)
+    want = a.copy()
+    ores = oracle.sort(want, k=k, base_case=B, trace=True)
+    t = dev(a)
+    gtr = ipls.sort_trace(t, k=k, base_case=B, key_type=kt_of(a))
+    assert host(t, a.dtype).tobytes() == want.tobytes()
+    compare_traces(gtr, ores)
+
+
 def test_worked_example_sort(ipls, golden):
     x = np.array([float(v) for v in golden("worked_example.txt")["input"][0]])
     t = dev(x)
