@@ -252,6 +252,15 @@ def test_tree_model_configs_scaled(ipls, name):
     compare_traces(gtr, ores)
 
 
+def test_tree_model_nan_rejected_unmodified(ipls):
+    a = np.random.default_rng(3).normal(0, 1, 300_000)
+    a[123_456] = np.nan
+    t = dev(a)
+    with pytest.raises(ipls.IPLSError):
+        ipls.sort(t, k=1024, model=ipls.MODEL_TREE)
+    assert host(t, np.float64).tobytes() == a.tobytes()
+
+
 def test_tree_model_rejects_k_not_power_of_two(ipls):
     t = dev(np.random.default_rng(0).random(10000))
     with pytest.raises(ipls.IPLSError):
