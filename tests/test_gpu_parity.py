@@ -256,8 +256,9 @@ def test_tree_model_nan_rejected_unmodified(ipls):
     a = np.random.default_rng(3).normal(0, 1, 300_000)
     a[123_456] = np.nan
     t = dev(a)
-    with pytest.raises(ipls.IPLSError):
-        ipls.sort(t, k=1024, model=ipls.MODEL_TREE)
+    with pytest.raises(ipls.IPLSError) as e:
+        ipls.sort(t, k=1024, key_type=ipls.KEY_F64, model=ipls.MODEL_TREE)
+    assert e.value.status == 2
     assert host(t, np.float64).tobytes() == a.tobytes()
 
 
