@@ -116,6 +116,39 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
                                  const ipls_model* h_model, uint64_t* d_offsets,
                                  uint16_t* d_bucket_ids, void* stream);
 
+/* ---- distributed top level (P:144-153 parallel sample sort) ----
+ * A global array is the concatenation, in rank order, of G ranks' device shards.  The
+ * exchange (paper_2208_06902_b200/distributed.py) is: (1) every rank writes the strata of
+ * the global level-0 sample it holds (ipls_sample_strata) and a SUM all-reduce assembles the
+ * whole sample; (2) every rank sorts it (ipls_sort_ex) and fits the same model
+ * (ipls_fit_fmcd); (3) every rank partitions its shard by that model (ipls_partition_level);
+ * (4) the per-rank bucket counts are all-gathered and ipls_assign_ranges gives rank r the
+ * contiguous buckets [bounds[r], bounds[r+1]); (5) one all-to-all moves the keys and every
+ * rank sorts what it received (ipls_sort_ex).  Rank r then holds the r-th key range. */
+
+/* S(m) = min(max(ceil(ceil(log2 m)/5) k - 1, 4), floor(m/2)) (R1, R19).  Host only. */
+uint32_t ipls_sample_size(uint64_t m, uint32_t k);
+
+/* Level-0 stratified sample (R2, R18: stratum j of [0, global_m) at level 0, begin 0,
+ * position lo_j + umulhi(h_j, hi_j - lo_j)) of the global array, restricted to this rank's
+ * positions [global_begin, global_begin + n_local).  d_keys: the rank's n_local keys
+ * (device).  d_sample: S uint64 slots (device, caller-owned); slot j receives the key's bits
+ * if this rank holds stratum j's position and is left untouched otherwise, so zero-filled
+ * buffers summed over ranks give exactly the sample a one-GPU ipls_sort of the concatenated
+ * array draws at level 0 (same seed).  S == 0: no-op.  Errors: INVALID_ARGUMENT (NULL
+ * pointers, S > global_m, the rank's range outside [0, global_m), global_m >= 2^48), CUDA. */
+ipls_status ipls_sample_strata(const void* d_keys, size_t n_local, uint64_t global_begin,
+                               uint64_t global_m, uint32_t S, uint64_t seed, uint64_t* d_sample,
+                               void* stream);
+
+/* Contiguous bucket ranges for G ranks balanced by count.  Host only.
+ * h_counts: k global bucket counts.  h_bounds: G+1 entries out; bounds[0] = 0, bounds[G] = k,
+ * nondecreasing; bounds[r] is the boundary b >= bounds[r-1] whose prefix count
+ * sum(counts[0..b)) is closest to r/G of the total (ties: the lower b).  Rank r receives
+ * buckets [bounds[r], bounds[r+1]).  Errors: INVALID_ARGUMENT (NULL, k == 0, G == 0). */
+ipls_status ipls_assign_ranges(const uint64_t* h_counts, uint32_t k, uint32_t G,
+                               uint32_t* h_bounds);
+
 /* ---- trace (tests and diagnostics) ---- */
 typedef struct {
   uint32_t level, kind;     /* level of the recursion; ipls_model_kind                      */

@@ -18,7 +18,7 @@ import numpy as np
 __all__ = [
     "IPLSError", "lib", "sort", "sort_host", "fit_fmcd", "partition_level", "sort_trace",
     "workspace_bytes", "Model", "Record", "KEY_F64", "KEY_U64", "MODEL_LINEAR", "MODEL_EQ3", "MODEL_TREE",
-    "DEFAULT_SEED", "launch_count",
+    "DEFAULT_SEED", "launch_count", "sample_size", "sample_strata", "assign_ranges",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -83,7 +83,7 @@ SYMBOLS = ["ipls_default_config", "ipls_sort_f64", "ipls_sort_u64", "ipls_sort_e
            "ipls_workspace_bytes", "ipls_sort_host", "ipls_fit_fmcd", "ipls_partition_level",
            "ipls_sort_trace", "ipls_status_string", "ipls_last_cuda_error",
            "ipls_kernel_launch_count", "ipls_profile_enable", "ipls_profile_reset",
-           "ipls_profile_read"]
+           "ipls_profile_read", "ipls_sample_size", "ipls_sample_strata", "ipls_assign_ranges"]
 
 _lib = None
 
@@ -119,6 +119,10 @@ def lib():
         L.ipls_profile_reset.argtypes = []; L.ipls_profile_reset.restype = None
         L.ipls_profile_read.argtypes = [ctypes.POINTER(_ProfEntry), sz]
         L.ipls_profile_read.restype = sz
+        L.ipls_sample_size.argtypes = [u64, u32]; L.ipls_sample_size.restype = u32
+        L.ipls_sample_strata.argtypes = [vp, sz, u64, u64, u32, u64, vp, vp]
+        L.ipls_sample_strata.restype = i32
+        L.ipls_assign_ranges.argtypes = [vp, u32, u32, vp]; L.ipls_assign_ranges.restype = i32
         _lib = L
     return _lib
 
@@ -259,6 +263,33 @@ def partition_level(keys_in, keys_out, model: Model, key_type: Optional[int] = N
                                       ids.data_ptr() if ids is not None else None,
                                       _stream(stream)))
     return off, (ids[:keys_in.numel()] if ids is not None else None)
+
+
+def sample_size(m: int, k: int) -> int:
+    """S(m) of P:473 (R1, R19), from the library (host function, no GPU needed)."""
+    return int(lib().ipls_sample_size(m, k))
+
+
+def sample_strata(keys, global_begin: int, global_m: int, S: int, out,
+                  seed: int = DEFAULT_SEED, stream=None) -> None:
+    """Write the strata of the global level-0 sample that this shard holds into `out`
+    (S int64 slots, CUDA; other slots untouched).  include/ipls.h: ipls_sample_strata."""
+    _check_tensor(keys)
+    _check_tensor(out)
+    if out.numel() < S:
+        raise ValueError("out must hold S slots")
+    _check(lib().ipls_sample_strata(keys.data_ptr(), keys.numel(), global_begin, global_m, S,
+                                    seed & 0xFFFFFFFFFFFFFFFF, out.data_ptr(), _stream(stream)))
+
+
+def assign_ranges(counts, G: int) -> List[int]:
+    """Contiguous bucket ranges per rank balanced by count (host; ipls_assign_ranges)."""
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.uint64))
+    if c.size == 0:
+        raise ValueError("counts must not be empty")
+    b = np.zeros(G + 1, dtype=np.uint32)
+    _check(lib().ipls_assign_ranges(c.ctypes.data, c.size, G, b.ctypes.data))
+    return [int(x) for x in b]
 
 
 @dataclass

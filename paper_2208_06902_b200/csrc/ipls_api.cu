@@ -731,6 +731,58 @@ ipls_status ipls_fit_fmcd(const void* d_sorted_sample, size_t S, ipls_key_type t
   }
 }
 
+uint32_t ipls_sample_size(uint64_t m, uint32_t k) { return sample_size(m, k); }
+
+ipls_status ipls_sample_strata(const void* d_keys, size_t n_local, uint64_t global_begin,
+                               uint64_t global_m, uint32_t S, uint64_t seed, uint64_t* d_sample,
+                               void* stream) {
+  if (S == 0) return IPLS_OK;
+  if (!d_sample || (n_local > 0 && !d_keys)) return IPLS_ERR_INVALID_ARGUMENT;
+  if (global_m >= (1ull << 48) || S > global_m || global_begin > global_m ||
+      n_local > global_m - global_begin)
+    return IPLS_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  try {
+    k_sample_strata<<<(S + 255) / 256, 256, 0, st>>>(static_cast<const uint64_t*>(d_keys),
+                                                     n_local, global_begin, global_m, S, seed,
+                                                     d_sample);
+    ck_launch();
+    ck(cudaStreamSynchronize(st));
+    return IPLS_OK;
+  } catch (const CudaFail& f) {
+    g_last_cuda_error = cudaGetErrorString(f.e);
+    return IPLS_ERR_CUDA;
+  }
+}
+
+ipls_status ipls_assign_ranges(const uint64_t* h_counts, uint32_t k, uint32_t G,
+                               uint32_t* h_bounds) {
+  if (!h_counts || !h_bounds || k == 0 || G == 0) return IPLS_ERR_INVALID_ARGUMENT;
+  unsigned __int128 total = 0;
+  for (uint32_t b = 0; b < k; ++b) total += h_counts[b];
+  h_bounds[0] = 0;
+  uint32_t b = 0;
+  unsigned __int128 pre = 0;  // keys in buckets [0, b)
+  for (uint32_t r = 1; r < G; ++r) {
+    // the boundary b >= bounds[r-1] whose prefix is closest to r/G of the keys (ties: lower)
+    const unsigned __int128 target = total * r;
+    auto dist = [&](unsigned __int128 p) {
+      const unsigned __int128 x = p * G;
+      return x > target ? x - target : target - x;
+    };
+    uint32_t best = b;
+    unsigned __int128 bestd = dist(pre), p = pre;
+    for (uint32_t c = b; c < k && p * G <= target; ++c) {  // past the target dist only grows
+      p += h_counts[c];
+      if (dist(p) < bestd) { bestd = dist(p); best = c + 1; }
+    }
+    while (b < best) pre += h_counts[b++];
+    h_bounds[r] = b;
+  }
+  h_bounds[G] = k;
+  return IPLS_OK;
+}
+
 ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_key_type t,
                                  const ipls_model* h_model, uint64_t* d_offsets,
                                  uint16_t* d_bucket_ids, void* stream) {

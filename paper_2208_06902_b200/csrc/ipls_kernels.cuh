@@ -2177,4 +2177,20 @@ __global__ void k_keys_to_ok(const uint64_t* __restrict__ in, uint64_t* __restri
     out[i] = f64 ? ok_of_f64(in[i]) : in[i];
 }
 
+// Distributed top level: the level-0 stratified sample
+// (R2, R18) of a global array of m keys of which this rank holds positions
+// [gbegin, gbegin + n).  Thread j computes stratum j's position exactly as the fit kernels do
+// for the root segment (level 0, begin 0) and copies the key if this rank holds it, so the
+// ranks' outputs, summed, are the sample a one-GPU sort of the concatenation draws.
+__global__ void k_sample_strata(const uint64_t* __restrict__ keys, uint64_t n, uint64_t gbegin,
+                                uint64_t m, uint32_t S, uint64_t seed,
+                                uint64_t* __restrict__ out) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= S) return;
+  const uint64_t t = sm64(sm64(sm64(seed) ^ 0ull) ^ 0ull);
+  const uint64_t lo = (uint64_t)j * m / S, hi = (uint64_t)(j + 1) * m / S;
+  const uint64_t idx = lo + __umul64hi(sm64(t ^ (uint64_t)j), hi - lo);
+  if (idx >= gbegin && idx - gbegin < n) out[j] = keys[idx - gbegin];
+}
+
 }  // namespace ipls

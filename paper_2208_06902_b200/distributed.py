@@ -1,0 +1,164 @@
+"""Multi-GPU top level of IPLS: one exchange step, then local sorts.
+
+The paper parallelises one distribution step across threads and recurses into buckets
+independently; across GPUs the same structure is the classic distributed sample
+sort.  A global array is the concatenation, in rank order, of every rank's shard:
+
+1. sample — each rank writes the strata of the global level-0 sample it holds
+   (`ipls_sample_strata`); a SUM all-reduce of the zero-filled slots assembles the whole
+   sample on every rank.  It is exactly the sample a one-GPU sort of the concatenation
+   draws at level 0 (R2, R18);
+2. fit — every rank sorts the sample (`ipls_sort_ex`) and fits FMCD (`ipls_fit_fmcd`,
+   Listing 1), so every rank holds the identical model (degenerate → EQ3, R5);
+3. partition — every rank partitions its shard by the model (`ipls_partition_level`,
+   P:505-530, stable);
+4. plan — the per-rank bucket counts are all-gathered; `ipls_assign_ranges` gives rank r the
+   contiguous buckets [bounds[r], bounds[r+1]) balanced by count (buckets are range-ordered,
+   so contiguous bucket ranges are key ranges);
+5. exchange + finish — one all-to-all moves every bucket range to its rank, and each rank
+   sorts what it received (`ipls_sort_ex`, the single-GPU path).
+
+Rank r then holds the r-th key range sorted; the concatenation over ranks is the sorted
+global array.  Every step that touches keys runs in libipls.so's kernels; this module only
+moves tensors between the C-ABI calls and the collectives (NCCL over NVLink on GPUs).  The
+compute steps are the `ops` object's methods so that the CPU `gloo` tests can run the same
+orchestration with the oracle standing in for the kernels (tests only; the product `ops`
+is `CudaOps`).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional
+
+import numpy as np
+
+from . import (DEFAULT_SEED, IPLSError, Model, assign_ranges, fit_fmcd, partition_level,
+               sample_size, sample_strata, sort, _key_type_of)
+
+
+class CudaOps:
+    """The product compute steps: libipls.so calls on CUDA tensors."""
+
+    def __init__(self, stream=None):
+        self.stream = stream
+
+    def sample(self, keys, global_begin: int, global_m: int, S: int, seed: int):
+        import torch
+        out = torch.zeros(S, dtype=torch.int64, device=keys.device)
+        sample_strata(keys, global_begin, global_m, S, out, seed=seed, stream=self.stream)
+        return out
+
+    def sort(self, keys, key_type: int, k: int, base_case: int, seed: int) -> int:
+        """Sort in place; returns the library status (0 = ok) instead of raising, so that
+        every rank can agree on the outcome before raising."""
+        try:
+            sort(keys, k=k, base_case=base_case, seed=seed, key_type=key_type,
+                 stream=self.stream)
+            return 0
+        except IPLSError as e:
+            return e.status
+
+    def fit(self, sorted_sample, key_type: int, k: int) -> Model:
+        return fit_fmcd(sorted_sample, k, key_type=key_type, stream=self.stream)
+
+    def partition(self, keys, model: Model, key_type: int):
+        """Returns (partitioned keys, offsets as a host list of k_eff + 1 ints)."""
+        import torch
+        out = torch.empty_like(keys)
+        off, _ = partition_level(keys, out, model, key_type=key_type, stream=self.stream)
+        return out, [int(x) for x in off.cpu().tolist()]
+
+
+@dataclass
+class DistResult:
+    keys: object            # this rank's sorted key range (same dtype/device as the input)
+    bounds: List[int]       # bucket ranges: rank r holds buckets [bounds[r], bounds[r+1])
+    model: Optional[Model]  # the shared top-level model (None when the global n < 8)
+    counts: np.ndarray      # global bucket counts of the top level
+    global_begin: int       # position of this rank's output in the sorted global array
+    global_n: int
+
+
+def _all_gather_int64(vals, group, device):
+    """All-gather a 1-D list of ints (same length on every rank) -> [G, len] numpy."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.int64, device=device)
+    G = dist.get_world_size(group)
+    parts = [torch.empty_like(t) for _ in range(G)]
+    dist.all_gather(parts, t, group=group)
+    return np.stack([p.cpu().numpy() for p in parts])
+
+
+def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SEED,
+              key_type: Optional[int] = None, group=None, ops=None,
+              marks: Optional[list] = None) -> DistResult:
+    """Sort the global array whose rank-ordered shards the ranks of `group` hold.
+
+    keys: this rank's shard (CUDA tensor, float64 or (u)int64 holding uint64 bits; left
+    unmodified).  Returns this rank's key range, sorted.  Raises IPLSError on every rank if
+    any rank's step fails (e.g. a NaN key anywhere: IPLS_ERR_NAN_KEY).
+    marks: optional list; (phase name, CUDA event) pairs are appended at the phase
+    boundaries (tools/time_dist.py).
+    """
+    import torch
+    import torch.distributed as dist
+    ops = ops if ops is not None else CudaOps()
+
+    def mark(name):
+        if marks is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append((name, e))
+    mark("start")
+    kt = _key_type_of(keys, key_type)
+    G = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    dev = keys.device
+    # collectives need the backend's device: NCCL takes CUDA tensors, gloo CPU ones
+    cdev = dev if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+    sizes = _all_gather_int64([keys.numel()], group, cdev)[:, 0]
+    gbegin, gm = int(sizes[:r].sum()), int(sizes.sum())
+    S = sample_size(gm, k) if gm >= 2 else 0
+
+    status = 0
+    model: Optional[Model] = None
+    if S >= 4:
+        smp = ops.sample(keys, gbegin, gm, S, seed)               # step 1
+        smp_c = smp.to(cdev)
+        dist.all_reduce(smp_c, op=dist.ReduceOp.SUM, group=group)
+        smp = smp_c.to(dev)
+        status = ops.sort(smp, kt, k, base_case, seed)            # step 2 (same on all ranks)
+        if status == 0:
+            model = ops.fit(smp, kt, k)
+    mark("sample+fit")
+    if model is not None:
+        part, off = ops.partition(keys, model, kt)               # step 3
+    else:                                                         # tiny input or NaN sample
+        part, off = keys, [0, keys.numel()]
+    part_w = part.view(torch.int64)
+    ke = len(off) - 1
+    cnt = _all_gather_int64([off[b + 1] - off[b] for b in range(ke)], group, cdev)
+    total = cnt.sum(axis=0)
+    mark("partition")
+    bounds = assign_ranges(total, G)                              # step 4
+    send = [off[bounds[d + 1]] - off[bounds[d]] for d in range(G)]
+    recv = [int(cnt[s, bounds[r]:bounds[r + 1]].sum()) for s in range(G)]
+    out_w = torch.empty(sum(recv), dtype=torch.int64, device=cdev)  # step 5
+    dist.all_to_all_single(out_w, part_w.to(cdev), output_split_sizes=recv,
+                           input_split_sizes=send, group=group)
+    out = out_w.to(dev).view(keys.dtype)
+    mark("plan+exchange")
+    if status == 0:
+        status = ops.sort(out, kt, k, base_case, seed)
+    mark("local sort")
+    st = torch.tensor([status], dtype=torch.int64, device=cdev)
+    dist.all_reduce(st, op=dist.ReduceOp.MAX, group=group)
+    if int(st.item()) != 0:
+        raise IPLSError(int(st.item()), "in the distributed sort")
+    below = int(sum(cnt[:, :bounds[r]].sum(axis=1))) if bounds[r] > 0 else 0
+    return DistResult(out, bounds, model, total, below, gm)
+
+
+__all__ = ["dist_sort", "DistResult", "CudaOps"]

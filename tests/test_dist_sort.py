@@ -1,0 +1,190 @@
+"""Distributed top level (paper_2208_06902_b200/distributed.py) over
+gloo with 2 and 3 CPU processes.
+
+The orchestration (sizes, sample all-reduce, count all-gather, `ipls_assign_ranges`, the
+all-to-all and the status agreement) is the product code; the per-rank compute steps are
+the oracle's (tests may use it; on GPUs `CudaOps` calls libipls.so).  Pins:
+
+* the concatenation of the ranks' outputs is the input sorted by ordering key;
+* the shared top-level model and the global bucket counts equal the oracle's level-0 record
+  of a one-process sort of the concatenated array (same strata, R2/R18), so the exchange
+  partitions the global array exactly as level 0 of the single-GPU method would;
+* every rank's range is the contiguous bucket range `assign_ranges` gave it;
+* a NaN anywhere raises on every rank.
+Also the host function `ipls_assign_ranges` against brute force.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.multiprocessing as mp  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import paper_2208_06902_b200 as ipls  # noqa: E402
+from paper_2208_06902_b200 import datagen  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class OracleOps:
+    """The per-rank compute steps done by the CPU oracle on CPU tensors (test stand-in)."""
+
+    @staticmethod
+    def _np(t, kt):
+        a = t.numpy().view(np.uint64)
+        return a.view(np.float64) if kt == ipls.KEY_F64 else a
+
+    def sample(self, keys, gbegin, gm, S, seed):
+        pos = oracle.sample_positions(seed, 0, 0, gm, S).astype(np.int64)
+        out = torch.zeros(S, dtype=torch.int64)
+        own = (pos >= gbegin) & (pos < gbegin + keys.numel())
+        bits = keys.view(torch.int64)
+        out[torch.from_numpy(np.nonzero(own)[0])] = bits[torch.from_numpy(pos[own] - gbegin)]
+        return out
+
+    def sort(self, t, kt, k, base_case, seed):
+        a = self._np(t, kt).copy()
+        r = oracle.sort(a, k=k, base_case=base_case, seed=seed)
+        if r.status == 0:
+            t.view(torch.int64).copy_(torch.from_numpy(a.view(np.int64)))
+        return r.status
+
+    def fit(self, s, kt, k):
+        a = self._np(s, kt)
+        f = oracle.fit_fmcd(a.astype(np.float64), k)
+        if f.degenerate:
+            piv = int(oracle.ordering_keys(a[a.size // 2: a.size // 2 + 1])[0])
+            return ipls.Model(0.0, 0.0, 3, 0, ipls.MODEL_EQ3, 0, piv, True)
+        return ipls.Model(f.A, f.B, k, f.D, ipls.MODEL_LINEAR, int(f.capped), 0, False)
+
+    def partition(self, keys, m, kt):
+        a = self._np(keys, kt)
+        out, off, _ = oracle.partition(a, m.a, m.b, m.k, m.kind, m.pivot_ok)
+        return torch.from_numpy(out.view(np.int64).copy()), [int(x) for x in off]
+
+
+def _shards(kind, n, G, seed):
+    rng = np.random.default_rng(seed)
+    a = datagen.fuzz_array(rng, n, "normal" if kind == "nan_one" else kind)
+    if kind == "nan_one":
+        a[(2 * n) // 3] = np.nan  # not a sampled position's concern: any NaN must raise
+    cuts = np.sort(rng.integers(0, n + 1, G - 1))
+    if G > 2:
+        cuts[0] = cuts[1]  # one empty shard
+    return a, np.split(a, cuts)
+
+
+def _worker(rank, world, port, q, kind, n, k, B, seed):
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    import torch.distributed as dist
+    from paper_2208_06902_b200.distributed import dist_sort
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _, shards = _shards(kind, n, world, seed)
+        mine = torch.from_numpy(shards[rank].view(np.int64).copy())
+        kt = ipls.KEY_F64 if shards[rank].dtype == np.float64 else ipls.KEY_U64
+        try:
+            res = dist_sort(mine, k=k, base_case=B, key_type=kt, ops=OracleOps())
+            m = res.model
+            q.put((rank, "ok", res.keys.numpy().copy(), res.bounds, res.counts,
+                   None if m is None else (m.a, m.b, m.D, m.kind, m.pivot_ok),
+                   res.global_begin, res.global_n))
+        except ipls.IPLSError as e:
+            q.put((rank, "err", e.status))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, kind, n, k=64, B=64, seed=3):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q, kind, n, k, B, seed))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(world):
+        v = q.get(timeout=300)
+        res[v[0]] = v
+    for p in ps:
+        p.join(120)
+        assert p.exitcode == 0
+    return [res[r] for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("kind", ["normal", "lognormal", "few_distinct", "u64_above_2_53",
+                                  "signed_zeros", "all_equal"])
+def test_dist_sort_matches_oracle_level0(world, kind):
+    n, k, B, seed = 30000, 64, 64, 3
+    a, _ = _shards(kind, n, world, seed)
+    res = _run(world, kind, n, k, B, seed)
+    assert all(r[1] == "ok" for r in res)
+    got = np.concatenate([r[2] for r in res]).view(a.dtype)
+    want = a[np.argsort(oracle.ordering_keys(a), kind="stable")]
+    assert got.tobytes() == want.tobytes()
+    ref = oracle.sort(a.copy(), k=k, base_case=B, trace=True)
+    r0 = ref.records[0]
+    bounds, counts, model = res[0][3], res[0][4], res[0][5]
+    assert all(r[3] == bounds and np.array_equal(r[4], counts) and r[5] == model for r in res)
+    assert np.array_equal(counts.astype(np.uint64), r0.counts)
+    if r0.kind == oracle.MODEL_LINEAR:
+        assert model[3] == ipls.MODEL_LINEAR
+        assert (model[0], model[1], model[2]) == (r0.A, r0.B, r0.D)
+    else:
+        assert model[3] == ipls.MODEL_EQ3 and model[4] == r0.pivot_ok
+    # rank r holds exactly the keys of buckets [bounds[r], bounds[r+1]) at its position
+    pre = np.concatenate([[0], np.cumsum(counts)])
+    for r in res:
+        rk = r[0]
+        assert r[6] == pre[bounds[rk]] and len(r[2]) == pre[bounds[rk + 1]] - pre[bounds[rk]]
+        assert r[7] == n
+
+
+def test_dist_sort_tiny_and_nan():
+    res = _run(2, "normal", 5)  # global n < 8: no sample, everything to one rank
+    assert all(r[1] == "ok" and r[5] is None for r in res)
+    a, _ = _shards("normal", 5, 2, 3)
+    got = np.concatenate([r[2] for r in res]).view(np.float64)
+    assert got.tobytes() == np.sort(a).tobytes()
+    res = _run(2, "nan_one", 20000)
+    assert all(r[1] == "err" and r[2] == 2 for r in res)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 5, 8])
+def test_assign_ranges_is_argmin_per_boundary(G):
+    rng = np.random.default_rng(G)
+    for trial in range(200):
+        k = int(rng.integers(1, 40))
+        c = rng.integers(0, 5, k) * (rng.random(k) < 0.7)
+        if trial % 7 == 0:
+            c[:] = 0
+            c[rng.integers(0, k)] = 100
+        b = ipls.assign_ranges(c, G)
+        assert b[0] == 0 and b[G] == k and all(b[i] <= b[i + 1] for i in range(G))
+        pre = np.concatenate([[0], np.cumsum(c)])
+        tot = int(pre[-1])
+        for r in range(1, G):
+            cand = range(b[r - 1], k + 1)
+            d = [abs(G * int(pre[x]) - r * tot) for x in cand]
+            assert b[r] == b[r - 1] + int(np.argmin(d))  # argmin, ties to the lower boundary
+
+
+def test_sample_size_matches_oracle():
+    for m in [2, 7, 8, 100, 4097, 10**6, 10**8, 2 * 10**8, 3 * 10**9]:
+        for k in [3, 64, 256, 1024]:
+            assert ipls.sample_size(m, k) == oracle.sample_size(m, k)

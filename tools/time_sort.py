@@ -17,6 +17,14 @@ for name in names:
     else:
         cfg = datagen.CONFIGS[name]
         a = datagen.generate(name)
+    order = os.environ.get("ORDER", "")  # presorted inputs: sorted, reverse, or G runs
+    if order == "sorted":
+        a = np.sort(a)
+    elif order == "reverse":
+        a = np.sort(a)[::-1].copy()
+    elif order.startswith("runs"):  # G sorted runs of a random split (what dist_sort's local
+        G = int(order[4:] or 8)       # sorts receive is G bucket-ordered runs)
+        a = np.concatenate([np.sort(x) for x in np.array_split(a, G)])
     kt = 0 if a.dtype == np.float64 else 1
     src = torch.from_numpy(a.view(np.int64)).cuda()
     t = torch.empty_like(src)
