@@ -1222,6 +1222,7 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
 #else
 #define SC_TICK(N)
 #endif
+  bool dense = false;  // block-uniform
   for (uint32_t t0 = 0; t0 < ch.len; t0 += kSTile4) {
     const uint32_t tl = min((uint32_t)kSTile4, ch.len - t0);
     {
@@ -1231,14 +1232,37 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
     __syncthreads();
     SC_TICK(0);
     uint32_t bl[kSRounds4];  // bucket | in-warp rank << 16
+    if (dense) {
+      // Few buckets per tile (presorted, clustered or EQ3 input): a warp whose keys share one
+      // bucket takes one atomic for all of them instead of 32 serialised same-address atomics.
 #pragma unroll
-    for (int r = 0; r < kSRounds4; ++r) {
-      const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
-      bl[r] = 0;
-      if (i < tl) {
-        const uint32_t b = bucket(key[r]);
-        const uint32_t loc = (atomicAdd(&wcw[b], winc) >> wsh) & 0xffffu;
-        bl[r] = b | (loc << 16);
+      for (int r = 0; r < kSRounds4; ++r) {
+        const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
+        const bool valid = i < tl;
+        const uint32_t b = valid ? bucket(key[r]) : 0u;
+        const uint32_t b0 = __shfl_sync(0xffffffffu, b, 0);
+        bl[r] = 0;
+        if (__all_sync(0xffffffffu, !valid || b == b0)) {
+          const uint32_t nv = __popc(__ballot_sync(0xffffffffu, valid));
+          uint32_t base = 0;
+          if (lane == 0 && nv) base = atomicAdd(&wcw[b0], nv * winc);
+          base = (__shfl_sync(0xffffffffu, base, 0) >> wsh) & 0xffffu;
+          if (valid) bl[r] = b | ((base + lane) << 16);
+        } else if (valid) {
+          const uint32_t loc = (atomicAdd(&wcw[b], winc) >> wsh) & 0xffffu;
+          bl[r] = b | (loc << 16);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < kSRounds4; ++r) {
+        const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
+        bl[r] = 0;
+        if (i < tl) {
+          const uint32_t b = bucket(key[r]);
+          const uint32_t loc = (atomicAdd(&wcw[b], winc) >> wsh) & 0xffffu;
+          bl[r] = b | (loc << 16);
+        }
       }
     }
     __syncthreads();
@@ -1282,7 +1306,9 @@ __device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_use
       }
       if (threadIdx.x == NT - 1) toff[k] = ex;
     }
-    __syncthreads();
+    static_assert(kSBpt == 1, "one bucket per thread in the tile statistics");
+    // next tile's path: dense when the tile's keys average >= 32 per non-empty bucket
+    dense = __syncthreads_count(cnt[0] != 0) * 32u <= tl;
     SC_TICK(2);
 #pragma unroll
     for (int r = 0; r < kSRounds4; ++r) {
@@ -1414,6 +1440,7 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
 #ifdef IPLS_SCATTER_TIMING
   long long t_prev_ = clock64();
 #endif
+  bool dense = false;  // block-uniform
   for (uint32_t t0 = 0; t0 < ch.len; t0 += kUTile) {
     const uint32_t tl = min((uint32_t)kUTile, ch.len - t0);
     for (uint32_t b = threadIdx.x; b < k; b += NT) cnt[b] = 0u;
@@ -1427,8 +1454,16 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
     for (int r = 0; r < kURounds; ++r) {
       const uint32_t i = wp * (kURounds * 32) + r * 32 + lane;
       uint32_t bb = 0xffffu;
-      if (i < tl) {
-        bb = bucket(key[r]);
+      if (i < tl) bb = bucket(key[r]);
+      if (dense) {  // as in the stable path: one atomic for a warp of one bucket
+        const uint32_t b0 = __shfl_sync(0xffffffffu, bb, 0);
+        if (__all_sync(0xffffffffu, bb == 0xffffu || bb == b0)) {
+          const uint32_t nv = __popc(__ballot_sync(0xffffffffu, bb != 0xffffu));
+          if (lane == 0 && nv) atomicAdd(&cnt[b0], nv);
+        } else if (bb != 0xffffu) {
+          atomicAdd(&cnt[bb], 1u);
+        }
+      } else if (bb != 0xffffu) {
         atomicAdd(&cnt[bb], 1u);
       }
       if (r & 1) bk[r >> 1] |= bb << 16;
@@ -1456,13 +1491,23 @@ __device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict_
         }
         ex += cc[q];
       }
+      dense = __syncthreads_count(cc[0] != 0) * 32u <= tl;  // this placement, next count
     }
-    __syncthreads();
     SC_TICK(13);
 #pragma unroll
     for (int r = 0; r < kURounds; ++r) {
       const uint32_t bb = (bk[r >> 1] >> (16 * (r & 1))) & 0xffffu;
-      if (bb != 0xffffu) {
+      const uint32_t b0 = dense ? __shfl_sync(0xffffffffu, bb, 0) : 0u;
+      if (dense && __all_sync(0xffffffffu, bb == 0xffffu || bb == b0)) {
+        const uint32_t nv = __popc(__ballot_sync(0xffffffffu, bb != 0xffffu));
+        uint32_t base = 0;
+        if (lane == 0 && nv) base = atomicAdd(&cur[b0], nv);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (bb != 0xffffu) {
+          stage[base + lane] = key[r];
+          if constexpr (MODE == (int)kModelTree) sbk[base + lane] = (uint16_t)bb;
+        }
+      } else if (bb != 0xffffu) {
         const uint32_t pos = atomicAdd(&cur[bb], 1u);
         stage[pos] = key[r];
         if constexpr (MODE == (int)kModelTree) sbk[pos] = (uint16_t)bb;

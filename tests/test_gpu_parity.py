@@ -159,6 +159,29 @@ def test_sort_parity_fuzz(ipls, kind, size):
     n, k, B = FUZZ_SIZES[size]
     rng = np.random.default_rng(size * 131 + len(kind))
     a = datagen.fuzz_array(rng, n, kind)
+    sort_parity_with_layouts(ipls, a, k, B)
+
+
+@pytest.mark.parametrize("order", ["sorted", "reverse", "runs8", "bucket_blocks"])
+@pytest.mark.parametrize("n,k", [(3_000_000, 256), (3_000_000, 1024), (1_500_007, 64)])
+def test_presorted_parity(ipls, order, n, k):
+    """Presorted inputs put whole warps of keys into one bucket: the scatters' dense-tile path
+    (one aggregated atomic per warp, K3) must keep the stable layouts bit-exact."""
+    rng = np.random.default_rng(n + k)
+    a = rng.normal(0, 1, n)
+    if order == "sorted":
+        a = np.sort(a)
+    elif order == "reverse":
+        a = np.sort(a)[::-1].copy()
+    elif order == "runs8":
+        a = np.concatenate([np.sort(x) for x in np.array_split(a, 8)])
+    else:  # what dist_sort's local sorts receive: coarse ranges in order, random inside
+        q = np.floor(a * 8).astype(np.int64)
+        a = a[np.argsort(q, kind="stable")]
+    sort_parity_with_layouts(ipls, a, k, 4096)
+
+
+def sort_parity_with_layouts(ipls, a, k, B):
     want = a.copy()
     ores = oracle.sort(want, k=k, base_case=B, trace=True, snapshots=True)
     t = dev(a)
