@@ -107,6 +107,12 @@ ipls_status ipls_sort_host(void* h_keys, size_t n, ipls_key_type t, const ipls_c
 ipls_status ipls_fit_fmcd(const void* d_sorted_sample, size_t S, ipls_key_type t, uint32_t k,
                           ipls_model* h_out, void* stream);
 
+/* As ipls_fit_fmcd for an UNSORTED sample: the fit kernel sorts the S keys by ordering key
+ * in shared memory first (the same CTA sort the sort's own fits use), then fits.
+ * Used by the multi-GPU top level (one launch instead of a sort call plus a fit call). */
+ipls_status ipls_fit_sample(const void* d_sample, size_t S, ipls_key_type t, uint32_t k,
+                            ipls_model* h_out, void* stream);
+
 /* One distribution step of a single segment with a caller-supplied model: classify every
  * key (evaluated as RN(RN(a*x) + b), no FMA, R7), histogram, prefix-sum and
  * stable scatter into contiguous buckets (R11).
@@ -175,6 +181,9 @@ ipls_status ipls_sort_trace(void* d_keys, size_t n, ipls_key_type t, const ipls_
 
 const char* ipls_status_string(ipls_status s);
 const char* ipls_last_cuda_error(void);
+/* Test hook: set the level counter whose low 16 bits tag the lookback status words (the
+ * regression test for stale words that look valid, tests/test_gpu_parity.py). */
+void ipls_debug_set_epoch(uint32_t e);
 /* Number of kernels the library enqueued since load (diagnostics / bench launch count). */
 uint64_t ipls_kernel_launch_count(void);
 

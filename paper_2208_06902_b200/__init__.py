@@ -83,7 +83,7 @@ SYMBOLS = ["ipls_default_config", "ipls_sort_f64", "ipls_sort_u64", "ipls_sort_e
            "ipls_workspace_bytes", "ipls_sort_host", "ipls_fit_fmcd", "ipls_partition_level",
            "ipls_sort_trace", "ipls_status_string", "ipls_last_cuda_error",
            "ipls_kernel_launch_count", "ipls_profile_enable", "ipls_profile_reset",
-           "ipls_profile_read", "ipls_sample_size", "ipls_sample_strata", "ipls_assign_ranges"]
+           "ipls_profile_read", "ipls_sample_size", "ipls_sample_strata", "ipls_assign_ranges", "ipls_fit_sample", "ipls_debug_set_epoch"]
 
 _lib = None
 
@@ -119,6 +119,9 @@ def lib():
         L.ipls_profile_reset.argtypes = []; L.ipls_profile_reset.restype = None
         L.ipls_profile_read.argtypes = [ctypes.POINTER(_ProfEntry), sz]
         L.ipls_profile_read.restype = sz
+        L.ipls_debug_set_epoch.argtypes = [u32]; L.ipls_debug_set_epoch.restype = None
+        L.ipls_fit_sample.argtypes = [vp, sz, i32, u32, ctypes.POINTER(_Model), vp]
+        L.ipls_fit_sample.restype = i32
         L.ipls_sample_size.argtypes = [u64, u32]; L.ipls_sample_size.restype = u32
         L.ipls_sample_strata.argtypes = [vp, sz, u64, u64, u32, u64, vp, vp]
         L.ipls_sample_strata.restype = i32
@@ -234,13 +237,16 @@ class Model:
     degenerate: bool = False
 
 
-def fit_fmcd(sorted_sample, k: int, key_type: Optional[int] = None, stream=None) -> Model:
-    """FMCD (Listing 1) of a sorted sample held in a CUDA tensor."""
+def fit_fmcd(sorted_sample, k: int, key_type: Optional[int] = None, stream=None,
+             presorted: bool = True) -> Model:
+    """FMCD (Listing 1) of a sample held in a CUDA tensor: sorted (ipls_fit_fmcd), or
+    presorted=False to have the fit kernel sort it first (ipls_fit_sample)."""
     _check_tensor(sorted_sample)
     kt = _key_type_of(sorted_sample, key_type)
     m = _Model()
-    st = lib().ipls_fit_fmcd(sorted_sample.data_ptr(), sorted_sample.numel(), kt, k,
-                             ctypes.byref(m), _stream(stream))
+    fn = lib().ipls_fit_sample if not presorted else lib().ipls_fit_fmcd
+    st = fn(sorted_sample.data_ptr(), sorted_sample.numel(), kt, k, ctypes.byref(m),
+            _stream(stream))
     if st not in (0, 3):
         _check(st)
     return Model(m.a, m.b, m.k, m.D, m.kind, m.capped, m.pivot_ok, st == 3)

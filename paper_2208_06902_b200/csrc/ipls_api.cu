@@ -397,7 +397,6 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     // per-level metadata, sized by this level's actual counts
     const MetaLayout ML = meta_layout(nseg, nchunk, nsample, k, p.tree);
     void* meta = d_meta_in;
-    bool clear_status = false;
     if (meta_cache) {
       meta_cache->ensure(ML.total);
       meta = meta_cache->ptr;
@@ -407,12 +406,16 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
       }
     } else {
       if (ML.total > meta_bytes_in) return IPLS_ERR_OUT_OF_MEMORY;
-      clear_status = true;  // caller memory: no history of epochs
     }
     bool wrapped = false;
     const uint32_t epoch = next_epoch(&wrapped);
-    if (clear_status || wrapped)
-      ck(cudaMemsetAsync(at<uint64_t>(meta, ML.status), 0, (size_t)nchunk * k * 8, st));
+    // The status region is cleared at EVERY level: the layout is sized per level, so this
+    // level's status words overlap what earlier levels (and calls) stored there — cref keys,
+    // prefixes — and a stale 64-bit word whose top 16 bits happen to equal the epoch tag would
+    // pass the lookback's validity test (an f64 key near 1.0 carries 0x3ff0 there).  ~2 us
+    // per level; the epoch tag still orders the words written within the level.
+    (void)wrapped;
+    ck(cudaMemsetAsync(at<uint64_t>(meta, ML.status), 0, (size_t)nchunk * k * 8, st));
     ModelDev* models = at<ModelDev>(meta, ML.models);
     uint64_t* samples = at<uint64_t>(meta, ML.samples);
     uint64_t* seg_dst = at<uint64_t>(meta, ML.seg_dst);
@@ -686,8 +689,21 @@ ipls_status ipls_sort_host(void* h_keys, size_t n, ipls_key_type t, const ipls_c
   }
 }
 
+static ipls_status fit_given(const void* d_sorted_sample, size_t S, ipls_key_type t, uint32_t k,
+                             ipls_model* h_out, void* stream, int sort_given);
+
 ipls_status ipls_fit_fmcd(const void* d_sorted_sample, size_t S, ipls_key_type t, uint32_t k,
                           ipls_model* h_out, void* stream) {
+  return fit_given(d_sorted_sample, S, t, k, h_out, stream, 0);
+}
+
+ipls_status ipls_fit_sample(const void* d_sample, size_t S, ipls_key_type t, uint32_t k,
+                            ipls_model* h_out, void* stream) {
+  return fit_given(d_sample, S, t, k, h_out, stream, 1);
+}
+
+static ipls_status fit_given(const void* d_sorted_sample, size_t S, ipls_key_type t, uint32_t k,
+                             ipls_model* h_out, void* stream, int sort_given) {
   if (!d_sorted_sample || !h_out) return IPLS_ERR_INVALID_ARGUMENT;
   if (S < 4 || S > (size_t)kFitMaxS || k < 3 || k > IPLS_MAX_K) return IPLS_ERR_INVALID_ARGUMENT;
   if (t != IPLS_KEY_F64 && t != IPLS_KEY_U64) return IPLS_ERR_INVALID_ARGUMENT;
@@ -711,12 +727,12 @@ ipls_status ipls_fit_fmcd(const void* d_sorted_sample, size_t S, ipls_key_type t
       set_attrs<true>();
       k_gather_fit<true><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, k, cap,
                                                                 nullptr, dmod, smp, nullptr,
-                                                                nullptr);
+                                                                nullptr, sort_given);
     } else {
       set_attrs<false>();
       k_gather_fit<false><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, k, cap,
                                                                  nullptr, dmod, smp, nullptr,
-                                                                 nullptr);
+                                                                 nullptr, sort_given);
     }
     ck_launch();
     ModelDev hm;
@@ -880,6 +896,8 @@ const char* ipls_status_string(ipls_status s) {
 const char* ipls_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
 
 uint64_t ipls_kernel_launch_count(void) { return g_launches.load(); }
+
+void ipls_debug_set_epoch(uint32_t e) { g_epoch.store(e); }
 
 #ifdef IPLS_SCATTER_TIMING
 // dev builds only (tools/phase_scatter.py): per-phase cycle sums of thread 0 of every CTA

@@ -245,7 +245,7 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
     uint32_t level, uint32_t k, uint32_t cap, uint64_t* __restrict__ samples_out,
     ModelDev* __restrict__ models, const uint64_t* __restrict__ presorted_ok,
-    const uint32_t* __restrict__ redo, uint64_t* __restrict__ tree) {
+    const uint32_t* __restrict__ redo, uint64_t* __restrict__ tree, int sort_given = 0) {
   if (redo && !redo[blockIdx.x]) return;  // fitted by k_fit_small
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* a = reinterpret_cast<uint64_t*>(smraw);   // cap
@@ -261,6 +261,7 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
   if (presorted_ok) {
     for (uint32_t j = threadIdx.x; j < S; j += kFitThreads) a[j] = presorted_ok[j];
     __syncthreads();
+    if (sort_given) block_sort_ok<kFitThreads>(a, tmp, fh, S, ss);  // ipls_fit_sample
   } else {
     const uint64_t t = sm64(sm64(sm64(seed) ^ (uint64_t)level) ^ sg.begin);
     StrataWalk sw(threadIdx.x, kFitThreads, sg.m, S);

@@ -8,7 +8,7 @@ sort.  A global array is the concatenation, in rank order, of every rank's shard
    (`ipls_sample_strata`); a SUM all-reduce of the zero-filled slots assembles the whole
    sample on every rank.  It is exactly the sample a one-GPU sort of the concatenation
    draws at level 0 (P:115, R2, R18);
-2. fit — every rank sorts the sample (`ipls_sort_ex`) and fits FMCD (`ipls_fit_fmcd`,
+2. fit — every rank sorts the sample and fits FMCD in one kernel (`ipls_fit_sample`,
    Listing 1, P:410-463), so every rank holds the identical model (degenerate → EQ3, R5);
 3. partition — every rank partitions its shard by the model (`ipls_partition_level`,
    P:505-530, stable);
@@ -58,8 +58,9 @@ class CudaOps:
         except IPLSError as e:
             return e.status
 
-    def fit(self, sorted_sample, key_type: int, k: int) -> Model:
-        return fit_fmcd(sorted_sample, k, key_type=key_type, stream=self.stream)
+    def fit(self, sample, key_type: int, k: int) -> Model:
+        """Sort the (unsorted) sample and fit FMCD in one launch (ipls_fit_sample)."""
+        return fit_fmcd(sample, k, key_type=key_type, stream=self.stream, presorted=False)
 
     def partition(self, keys, model: Model, key_type: int):
         """Returns (partitioned keys, offsets as a host list of k_eff + 1 ints)."""
@@ -129,13 +130,11 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
         smp_c = smp.to(cdev)
         dist.all_reduce(smp_c, op=dist.ReduceOp.SUM, group=group)
         smp = smp_c.to(dev)
-        status = ops.sort(smp, kt, k, base_case, seed)            # step 2 (same on all ranks)
-        if status == 0:
-            model = ops.fit(smp, kt, k)
+        model = ops.fit(smp, kt, k)                               # step 2 (same on all ranks)
     mark("sample+fit")
     if model is not None:
         part, off = ops.partition(keys, model, kt)               # step 3
-    else:                                                         # tiny input or NaN sample
+    else:                                                         # global n < 8
         part, off = keys, [0, keys.numel()]
     part_w = part.view(torch.int64)
     ke = len(off) - 1

@@ -64,6 +64,7 @@ class OracleOps:
 
     def fit(self, s, kt, k):
         a = self._np(s, kt)
+        a = a[np.argsort(oracle.ordering_keys(a), kind="stable")]  # the sample arrives unsorted
         f = oracle.fit_fmcd(a.astype(np.float64), k)
         if f.degenerate:
             piv = int(oracle.ordering_keys(a[a.size // 2: a.size // 2 + 1])[0])

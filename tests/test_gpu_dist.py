@@ -118,3 +118,20 @@ def test_dist_sort_nan_raises(ipls, nccl1):
     with pytest.raises(ipls.IPLSError) as e:
         dist_sort(dev(a).view(torch.float64))
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("S,k,kind", [(6143, 1024, "normal"), (4095, 256, "lognormal"),
+                                      (100, 10, "few_distinct"), (5119, 1024, "all_equal"),
+                                      (8192, 1024, "u64_above_2_53")])
+def test_fit_sample_unsorted_equals_oracle_fit(ipls, S, k, kind):
+    """ipls_fit_sample sorts the given sample in the fit kernel: same model as the oracle's
+    Listing 1 on the sorted sample (degenerate -> EQ3 with the sorted sample's median)."""
+    a = datagen.fuzz_array(np.random.default_rng(S + k), S, kind)
+    m = ipls.fit_fmcd(dev(a), k, key_type=0 if a.dtype == np.float64 else 1, presorted=False)
+    s = a[np.argsort(oracle.ordering_keys(a), kind="stable")]
+    f = oracle.fit_fmcd(s.astype(np.float64), k)
+    if f.degenerate:
+        assert m.degenerate and m.kind == ipls.MODEL_EQ3
+        assert m.pivot_ok == int(oracle.ordering_keys(s[S // 2:S // 2 + 1])[0])
+    else:
+        assert (m.a, m.b, m.D, bool(m.capped)) == (f.A, f.B, f.D, f.capped)

@@ -522,3 +522,24 @@ def test_concurrent_streams_threads(ipls):
     assert not errs, errs
     for t, w, a in zip(ts, wants, arrays):
         assert host(t, a.dtype).tobytes() == w.tobytes()
+
+
+@pytest.mark.parametrize("tag", [0x3FF0, 0xBFF0])
+def test_stale_status_words_cannot_pass_the_epoch_check(ipls, tag):
+    """Regression: a level's lookback status words overlap what earlier levels stored in the
+    same metadata (first keys of homogeneous buckets, prefixes).  A stale key whose top 16 bits
+    equal the level's epoch tag (and whose bits 46-47 are set) looked like a valid status word,
+    giving wrong prefixes (wrong output, illegal addresses; tools/epoch_collision.py).  The
+    status region is now cleared every level; epochs are forced onto the keys' tag here."""
+    rng = np.random.default_rng(tag)
+    base = np.uint64(tag) << np.uint64(48)
+    vals = (base | (np.uint64(3) << np.uint64(46)) |
+            rng.integers(0, 1 << 20, 40).astype(np.uint64)).view(np.float64)
+    a = np.concatenate([vals[rng.integers(0, vals.size, 3_000_000)], rng.normal(0, 1, 1_000_000)])
+    rng.shuffle(a)
+    want = np.sort(a)
+    for e0 in range(tag - 3, tag + 1):
+        ipls.lib().ipls_debug_set_epoch(e0)
+        t = dev(a)
+        ipls.sort(t, k=1024, base_case=4096, key_type=0)
+        assert host(t, np.float64).tobytes() == want.tobytes(), f"epoch {e0:#x}"

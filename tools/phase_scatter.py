@@ -14,6 +14,8 @@ from paper_2208_06902_b200 import datagen
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 cfg = datagen.CONFIGS[name]
 a = datagen.generate(name)
+if os.environ.get("ORDER") == "sorted":  # presorted input (K3, dense tiles)
+    a = np.sort(a)
 kt = 0 if a.dtype == np.float64 else 1
 src = torch.from_numpy(a.view(np.int64)).cuda()
 t = torch.empty_like(src)
