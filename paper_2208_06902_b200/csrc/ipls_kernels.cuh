@@ -1116,7 +1116,8 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
   }
   // ---- decoupled lookback over the chunks of this segment, bucket by bucket ----
   // One 64-bit status word per (chunk, bucket): AGG (own count) or INC (inclusive prefix),
-  // tagged with the level's epoch, so the status array needs no clearing between levels.
+  // tagged with the level's epoch; the host clears the status region before every level (a
+  // stale word of another array could otherwise carry the current tag).
   const bool first = (c == sg.chunk_first);
   const bool last = (c == sg.chunk_first + sg.nchunks - 1);
   uint32_t tot[kCBpt];
