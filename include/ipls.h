@@ -142,7 +142,8 @@ uint32_t ipls_sample_size(uint64_t m, uint32_t k);
  * if this rank holds stratum j's position and is left untouched otherwise, so zero-filled
  * buffers summed over ranks give exactly the sample a one-GPU ipls_sort of the concatenated
  * array draws at level 0 (same seed).  S == 0: no-op.  Errors: INVALID_ARGUMENT (NULL
- * pointers, S > global_m, the rank's range outside [0, global_m), global_m >= 2^48), CUDA. */
+ * pointers, S > global_m, S > 8192 (the largest sample the fit kernels take), the rank's range
+ * outside [0, global_m), global_m >= 2^48), CUDA. */
 ipls_status ipls_sample_strata(const void* d_keys, size_t n_local, uint64_t global_begin,
                                uint64_t global_m, uint32_t S, uint64_t seed, uint64_t* d_sample,
                                void* stream);
@@ -184,6 +185,11 @@ const char* ipls_last_cuda_error(void);
 /* Test hook: set the level counter whose low 16 bits tag the lookback status words (the
  * regression test for stale words that look valid, tests/test_gpu_parity.py). */
 void ipls_debug_set_epoch(uint32_t e);
+/* Test hook: on != 0 makes every CTA of the stable scatter rank keys with match.any peer
+ * masks (stable by construction), the path it otherwise takes only if its probe finds that
+ * same-address lanes of a shared-memory atomic are not served in lane order (DESIGN.md §5,
+ * K3).  Applies to the current device; 0 restores the default. */
+void ipls_debug_force_match_rank(int on);
 /* Number of kernels the library enqueued since load (diagnostics / bench launch count). */
 uint64_t ipls_kernel_launch_count(void);
 

@@ -14,6 +14,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -180,7 +181,7 @@ FixedLayout fixed_layout(const Params& p) {
 // Per-level metadata (sized by the level's actual counts).  `status` comes first so a fresh
 // allocation can be cleared cheaply.
 struct MetaLayout {
-  size_t status, cflag, cref, chunk_pre, models, samples, seg_dst, seg_tot, seg_done, seg_term,
+  size_t status, cflag, cref, chunk_pre, models, samples, seg_dst, seg_tot, seg_term,
       tree, total;
 };
 
@@ -197,7 +198,6 @@ MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_
   L.samples = take(samples * 8 + 64);
   L.seg_dst = take(segs * k * 8);
   L.seg_tot = take(segs * k * 4);
-  L.seg_done = take(segs * 4);
   L.seg_term = take(segs * 4);
   L.tree = take(tree ? segs * kMaxK * 8 : 0);  // splitter heaps (8 KB per segment)
   L.total = o;
@@ -265,14 +265,28 @@ struct TraceSink {
   std::vector<std::vector<uint64_t>> counts, samples;
 };
 
+size_t scatter_stable_smem(uint32_t k) { return scatter_stable_smem_bytes(k); }
+size_t scatter_term_smem(uint32_t k) { return scatter_term_smem_bytes(k); }
+
+// Both scatter kernels over the level's chunks: each one takes its own kind of chunk (stable
+// or terminal, known on the device after K2) and returns at once for the other.
 template <bool F64>
 void launch_scatter(uint32_t nchunk, cudaStream_t st, const LevelArgs& la, uint64_t* user,
-                    uint64_t* scr, bool tree = false) {
-  const size_t smem = std::max(scatter_smem_bytes(la.k), scatter_unstable_smem_bytes(la.k));
+                    uint64_t* scr, bool tree = false, bool stable_only = false) {
+  {
+  IPLS_PROF("scatter_stable", 0);
   if (tree)
-    k_scatter<F64, true><<<nchunk, kSThreads4, smem, st>>>(la, user, scr);
+    k_scatter_stable<F64, true><<<nchunk, kSThreads, scatter_stable_smem(la.k), st>>>(la, user, scr);
   else
-    k_scatter<F64, false><<<nchunk, kSThreads4, smem, st>>>(la, user, scr);
+    k_scatter_stable<F64, false><<<nchunk, kSThreads, scatter_stable_smem(la.k), st>>>(la, user, scr);
+  ck_launch();
+  }
+  if (stable_only) return;
+  IPLS_PROF("scatter_term", 0);
+  if (tree)
+    k_scatter_term<F64, true><<<nchunk, kTThreads, scatter_term_smem(la.k), st>>>(la, user, scr);
+  else
+    k_scatter_term<F64, false><<<nchunk, kTThreads, scatter_term_smem(la.k), st>>>(la, user, scr);
   ck_launch();
 }
 template <bool F64>
@@ -288,14 +302,11 @@ void launch_classify(uint32_t nchunk, cudaStream_t st, const LevelArgs& la, bool
 }
 size_t warp_base_smem() { return kWBSmemPerWarp * kWBWarps; }
 size_t base_smem() { return kBCSmem; }
-int g_num_sms = 0;
 uint32_t num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    ck(cudaGetDevice(&dev));
-    ck(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  return (uint32_t)g_num_sms;
+  int dev = 0, n = 0;
+  ck(cudaGetDevice(&dev));
+  ck(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  return (uint32_t)n;
 }
 uint32_t fit_cap(uint32_t maxS) {
   uint32_t c = 64;
@@ -304,10 +315,16 @@ uint32_t fit_cap(uint32_t maxS) {
 }
 size_t fit_smem(uint32_t cap) { return (size_t)cap * 20; }
 
+// The dynamic-smem limits are per (device context, kernel): set once per device, under a
+// lock (first calls may race from several threads).
 template <bool F64>
 void set_attrs() {
-  static bool done = false;
-  if (done) return;
+  int dev = 0;
+  ck(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::set<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(dev)) return;
   ck(cudaFuncSetAttribute(k_gather_fit<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)fit_smem(kFitMaxS)));
   ck(cudaFuncSetAttribute(k_fit_small<F64, kFSThreads, kFSItems>,
@@ -325,14 +342,16 @@ void set_attrs() {
   for (int tr = 0; tr < 2; ++tr) {
     ck(cudaFuncSetAttribute(tr ? k_classify_scan<F64, true> : k_classify_scan<F64, false>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)classify_smem(kMaxK)));
-    ck(cudaFuncSetAttribute(tr ? k_scatter<F64, true> : k_scatter<F64, false>,
+    ck(cudaFuncSetAttribute(tr ? k_scatter_stable<F64, true> : k_scatter_stable<F64, false>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)std::max({scatter_smem_bytes(kMaxK),
-                                           scatter_unstable_smem_bytes(kMaxK),
-                                           win_scratch_bytes(kMaxK)})));
+                            (int)scatter_stable_smem(kMaxK)));
+    ck(cudaFuncSetAttribute(tr ? k_scatter_term<F64, true> : k_scatter_term<F64, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)scatter_term_smem(kMaxK)));
+    ck(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)win_scratch_bytes(kMaxK)));
   }
-
-  done = true;
+  done.insert(dev);
 }
 
 uint32_t next_epoch(bool* wrapped) {
@@ -424,7 +443,6 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     uint64_t* tree = p.tree ? at<uint64_t>(meta, ML.tree) : nullptr;
 
     ck(cudaMemsetAsync(nctr, 0, sizeof(LevelCounters), st));
-    ck(cudaMemsetAsync(at<uint32_t>(meta, ML.seg_done), 0, (size_t)nseg * 4, st));
     {
       IPLS_PROF("gather_fit", 0);
       const uint32_t cap = fit_cap(max_S);
@@ -445,12 +463,11 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     }
     LevelArgs la{};
     la.src = src; la.segs = segs; la.chunks = chunks; la.models = models;
-    la.k = k; la.base_case = p.B; la.level = level; la.chunk_keys = p.chunk_keys;
+    la.k = k; la.base_case = p.B; la.level = level; la.chunk_keys = p.chunk_keys; la.nkeys = n;
     la.ticket = &cctr->ticket;
     la.status = at<uint64_t>(meta, ML.status);
     la.cflag = at<uint8_t>(meta, ML.cflag);
     la.cref = at<uint64_t>(meta, ML.cref);
-    la.seg_done = at<uint32_t>(meta, ML.seg_done);
     la.seg_term = at<uint32_t>(meta, ML.seg_term);
     la.chunk_pre = chunk_pre;
     la.seg_dst = seg_dst;
@@ -473,6 +490,11 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     {
       IPLS_PROF("scatter", 16.0 * level_keys);
       launch_scatter<F64>(nchunk, st, la, keys, scr, p.tree);
+    }
+    {
+      IPLS_PROF("emit", 0);
+      k_emit<<<nseg, kEThreads, win_scratch_bytes(k), st>>>(la);
+      ck_launch();
     }
 
     if (trace) {
@@ -754,6 +776,8 @@ ipls_status ipls_sample_strata(const void* d_keys, size_t n_local, uint64_t glob
                                void* stream) {
   if (S == 0) return IPLS_OK;
   if (!d_sample || (n_local > 0 && !d_keys)) return IPLS_ERR_INVALID_ARGUMENT;
+  // S is a level-0 sample size (<= kFitMaxS): j * m below stays inside 64 bits
+  if (S > (uint32_t)kFitMaxS) return IPLS_ERR_INVALID_ARGUMENT;
   if (global_m >= (1ull << 48) || S > global_m || global_begin > global_m ||
       n_local > global_m - global_begin)
     return IPLS_ERR_INVALID_ARGUMENT;
@@ -847,12 +871,11 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
     ck_launch();
     LevelArgs la{};
     la.src = static_cast<const uint64_t*>(d_in); la.segs = dseg; la.chunks = dch;
-    la.models = dmod; la.k = k; la.base_case = 0; la.level = 0; la.chunk_keys = ck_keys;
+    la.models = dmod; la.k = k; la.base_case = 0; la.level = 0; la.chunk_keys = ck_keys; la.nkeys = n;
     la.ticket = &dctr->ticket;
     la.status = at<uint64_t>(meta, ML.status);
     la.cflag = at<uint8_t>(meta, ML.cflag);
     la.cref = at<uint64_t>(meta, ML.cref);
-    la.seg_done = at<uint32_t>(meta, ML.seg_done);
     la.seg_term = at<uint32_t>(meta, ML.seg_term);
     la.chunk_pre = at<uint32_t>(meta, ML.chunk_pre);
     la.seg_dst = at<uint64_t>(meta, ML.seg_dst);
@@ -868,8 +891,7 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
       constexpr bool F64 = decltype(f64tag)::value;
       set_attrs<F64>();
       launch_classify<F64>(nchunk, st, la);
-      ck_launch();
-      launch_scatter<F64>(nchunk, st, la, out, out);
+      launch_scatter<F64>(nchunk, st, la, out, out, false, true);
     };
     if (t == IPLS_KEY_F64) body(std::true_type{}); else body(std::false_type{});
     ck(cudaStreamSynchronize(st));
@@ -898,6 +920,11 @@ const char* ipls_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
 uint64_t ipls_kernel_launch_count(void) { return g_launches.load(); }
 
 void ipls_debug_set_epoch(uint32_t e) { g_epoch.store(e); }
+
+void ipls_debug_force_match_rank(int on) {
+  const int v = on ? 1 : 0;
+  cudaMemcpyToSymbol(g_force_match_rank, &v, sizeof(v));
+}
 
 #ifdef IPLS_SCATTER_TIMING
 // dev builds only (tools/phase_scatter.py): per-phase cycle sums of thread 0 of every CTA

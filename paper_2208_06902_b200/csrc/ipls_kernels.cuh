@@ -13,6 +13,8 @@
 //                     work, the base-case windows and the fills (segment_emit)
 // After the level: k_base_warp / k_base_sort (base case) and k_fill.
 #pragma once
+#include <type_traits>
+
 #include "ipls_device.cuh"
 
 namespace ipls {
@@ -49,7 +51,10 @@ constexpr int kWBBins = kWBBinsPerKey * kWBCap;  // fine bins per warp
 constexpr int kWBWarps = IPLS_WB_WARPS;          // warps per CTA, one CTA per SM
 constexpr int kWBStride = kWBCap + 4;            // keys per prefetch buffer (+ alignment slack)
 constexpr int kWBItems = kWBCap / 32;            // keys per lane (held in registers)
-constexpr size_t kWBSmemPerWarp = (size_t)2 * kWBStride * 8 + (size_t)(kWBBins + 32) * 4;
+constexpr int kWBBpl = kWBBins / 32;             // bins per lane in the scan (16)
+constexpr int kWBBinWords = kWBBins + kWBBins / 8;  // bins with 4 pad words per 32
+constexpr size_t kWBSmemPerWarp = (size_t)2 * kWBStride * 8 + (size_t)kWBBinWords * 4;
+__device__ __forceinline__ uint32_t wb_phys(uint32_t f) { return f + ((f >> 5) << 2); }
 constexpr uint32_t kFineOverflow = 32;          // fine-bin load that triggers the bitonic fallback
 
 // ------------------------------------------------------------------------------------
@@ -673,6 +678,7 @@ struct LevelArgs {
   const ChunkDesc* chunks;
   const ModelDev* models;
   uint32_t k, base_case, level, chunk_keys;
+  uint64_t nkeys;        // length of the arrays (src and both destinations)
   uint32_t* ticket;
   uint64_t* status;      // [chunk][k]: epoch<<48 | state<<46 | count
   uint32_t* chunk_pre;   // [chunk][k] exclusive prefix within the segment
@@ -680,7 +686,6 @@ struct LevelArgs {
   uint32_t* seg_tot;     // [seg][k]   child counts
   uint8_t* cflag;        // [chunk][k] scatter homogeneity flag: 0 empty, 1 one value, 2 several
   uint64_t* cref;        // [chunk][k] the chunk's value of a one-value bucket
-  uint32_t* seg_done;    // [seg]      chunks of the segment scattered so far
   uint32_t* seg_term;    // [seg]      1: every child <= base case (terminal segment)
   uint32_t epoch;
   uint32_t* err;
@@ -708,6 +713,15 @@ __device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint32_t st, uin
          (uint64_t)cnt;
 }
 
+
+// Adds every thread's v into *dst with one atomic per warp (the level's key counters only feed
+// the per-kernel byte counts; one atomic per item would serialise every CTA of the level on
+// one L2 address).
+__device__ __forceinline__ void warp_add_u64(unsigned long long* dst, unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
 
 __device__ void emit_segment(const LevelArgs& a, uint64_t begin, uint32_t m, uint32_t flags,
                              uint32_t seg_idx, uint32_t samp_off, uint32_t ch_off) {
@@ -832,6 +846,7 @@ __device__ void pack_windows(const LevelArgs& a, const SegDesc& sg, uint32_t k,
   uint32_t w_off = block_exclusive_scan<NT>(nw, os.warp, &t_w);
   if (threadIdx.x == 0) os.res[4] = atomicAdd(cnt, t_w);
   __syncthreads();
+  unsigned long long wkeys = 0;
 #pragma unroll
   for (int q = 0; q < BPT; ++q) {
     if (sel[q] && w_mark[bb[q]]) {
@@ -842,12 +857,13 @@ __device__ void pack_windows(const LevelArgs& a, const SegDesc& sg, uint32_t k,
         wv.len = w_end[w_jump[bb[q]]] - base[q];
         wv.buf = dstbuf;
         out[gi] = wv;
-        atomicAdd((unsigned long long*)keys, (unsigned long long)wv.len);
+        wkeys += wv.len;
       } else {
         atomicOr(a.err, kErrOverflow);
       }
     }
   }
+  warp_add_u64((unsigned long long*)keys, wkeys);
   __syncthreads();  // scratch is reused by the next packing
 }
 
@@ -974,17 +990,19 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
       if (threadIdx.x == 0) atomicOr(a.err, kErrOverflow);
     } else {
       uint32_t i_seg = os.res[0] + o_seg, i_samp = os.res[1] + o_samp, i_ch = os.res[2] + o_ch;
+      unsigned long long nkeys = 0;
 #pragma unroll
       for (int q = 0; q < BPT; ++q) {
         if (cm[q]) {
           uint64_t cb = stuck ? sg.begin : sg.begin + base[q];
           emit_segment(a, cb, cm[q], stuck ? kSegForceEq3 : 0u, i_seg, i_samp, i_ch);
-          atomicAdd((unsigned long long*)&a.nctr->keys, (unsigned long long)cm[q]);
+          nkeys += cm[q];
           i_seg += 1;
           i_samp += sample_size(cm[q], k);
           i_ch += (cm[q] + a.chunk_keys - 1) / a.chunk_keys;
         }
       }
+      warp_add_u64((unsigned long long*)&a.nctr->keys, nkeys);
     }
   }
   if (stuck) return;  // block-uniform
@@ -1012,6 +1030,7 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
   uint32_t o_fill = block_exclusive_scan<NT>(nf, os.warp, &t_fill);
   if (threadIdx.x == 0 && t_fill) os.res[5] = atomicAdd(&a.nctr->n_fills, t_fill);
   __syncthreads();
+  unsigned long long fkeys = 0;
 #pragma unroll
   for (int q = 0; q < BPT; ++q) {
     if (cls[q] == 3 && dstbuf == 1) {
@@ -1020,12 +1039,13 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
         Fill f;
         f.begin = sg.begin + base[q]; f.len = tot[q]; f.value = rep[q]; f.pad = 0;
         a.fills[gi] = f;
-        atomicAdd((unsigned long long*)&a.nctr->fill_keys, (unsigned long long)tot[q]);
+        fkeys += tot[q];
       } else {
         atomicOr(a.err, kErrOverflow);
       }
     }
   }
+  warp_add_u64((unsigned long long*)&a.nctr->fill_keys, fkeys);
 }
 
 // Tile loop of phase 4a with the model kind and the optional outputs fixed at compile time.
@@ -1155,430 +1175,632 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
 }
 
 // ------------------------------------------------------------------------------------
-// Phase 4b: stable scatter of one chunk (R11), 1024 threads, 1 CTA per SM.
+// Phase 4b: scatter of one chunk into its segment's children (R11).
 //
-// Tile = 8192 keys; warp w owns keys [256w, 256w+256) in 8 rounds of 32.
-// Rank: every key does one smem atomicAdd on its warp's counter for its bucket (u16 halves
-// of packed u32 words, two warps per word).  Same-address lanes of one atomic instruction
-// are served in lane order on B200 (tools/micro/atom_order.cu: 0 violations in 2.2e9 lane
-// pairs), so the returned values are the stable in-warp ranks; a cross-warp scan and a scan
-// over buckets place every key in a bucket-sorted smem tile.  Stability is VERIFIED on the
-// staged tile (tile index must increase inside every bucket run) while it is written out,
-// and any offending run is rewritten in index order afterwards, so the layout is stable by
-// construction whatever the hardware does.
-// Write-out: key q of the staged tile goes to run_address[bucket] + 8 (q - tile_offset[bucket]);
-// a warp's 32 consecutive staged keys cover a few runs, so stores coalesce per run and the
-// L2 completes sectors shared by consecutive tiles before they are written back.
-// Homogeneity (R9): every key is compared with the first key of its bucket in the tile; the
-// per-bucket pass after the write-out compares that key with the chunk's first key of the
-// bucket.  The chunk's flags (0 empty, 1 one value, 2 several) and values go to global memory
-// for segment_emit.
-constexpr int kSThreads4 = 1024;
-constexpr int kSWarps4 = kSThreads4 / 32;          // 32
-constexpr int kSRounds4 = 8;                       // keys per thread per tile
-constexpr int kSBpt = kMaxK / kSThreads4;          // buckets per thread in the scans
-constexpr int kSTile4 = kSThreads4 * kSRounds4;    // 8192
-constexpr int kSPairs4 = kSWarps4 / 2;             // warp pairs sharing a counter word
+// Two kernels of 512 threads with tiles of kSTile = 8192 keys (16 per thread, in registers;
+// warp w owns keys [512 w, 512 w + 512) of the tile and item r of lane l is key
+// 512 w + 32 r + l, so every load is one coalesced 256-byte warp access):
+//   k_scatter_stable  chunks of segments with a child above the base case: those children are
+//                     sampled by position at the next level, so the layout is the stable one
+//                     (R11); 1 CTA per SM.
+//   k_scatter_term    chunks of terminal segments (every child <= base case): the children go
+//                     to the base case, an exact sort, so their interior order is free;
+//                     2 CTAs per SM.
+// Each kernel returns at once for the other kind of chunk; a segment's chunks are all of one
+// kind.  The CTA that completes a segment's last chunk runs segment_emit.
+//
+// Per tile: (A) ranks, (B) per-bucket offsets, (C) placement into a bucket-sorted smem stage,
+// (D) write-out of the stage.  Staged key q of bucket b goes to adjo[b] + q, adjo[b] = the
+// absolute position of bucket b's next key minus the run's start in the stage: a warp's 32
+// consecutive staged keys cover a few runs, so the stores coalesce per run.  Stores carry an
+// L2 evict_last policy so that lines of runs still open survive until the next tile completes
+// them.
+//
+// Cost model.  Both kernels are bound by the shared-memory (LSU) pipe, ~1 wavefront per clock
+// per SM, and its latency, not by instruction issue (ncu, profiles/r02_*).  So the write-out
+// recomputes a staged key's bucket (two FP64 ops) instead of staging it (a random 4-byte
+// store and a load), and a key's staged predecessor comes from the neighbouring lane by
+// shuffle instead of a second load.
+//
+// Stable rank (k_scatter_stable).  Every key does one shared-memory atomicAdd with return on
+// its warp's 16-bit counter for its bucket (two warps share a 32-bit word); the per-bucket
+// prefix over the warps (B) completes it.  The returned value is the key's rank among the
+// warp's earlier keys of its bucket if same-address lanes of one atomic are served in lane
+// order.  B200 does that (tools/micro/atom_order.cu: 0 violations in 2.2e9 lane pairs), but
+// the PTX model does not promise it, so every CTA first probes it on a few lane patterns
+// (atomic_lane_order_ok) and ranks with match.any peer masks if the probe fails: the leader of
+// each group of same-bucket lanes does one atomic for the group and the others add their
+// popcount rank -- stable by construction.  That path is the fallback, not the default,
+// because match.any serialises per distinct value: tools/micro/rank.cu measures 2.2 T keys/s
+// for the atomic rank, 0.26 T for a 10-ballot peer mask and 0.15 T for match.any, against
+// ~0.4 T keys/s for one pass at HBM speed.  ipls_debug_force_match_rank forces the fallback
+// (the tests run both).
+//
+// Homogeneity (R9, stable kernel only): a staged key that differs from its staged predecessor
+// of the same bucket marks the bucket "several values"; the first key of every bucket run in
+// a tile is compared with the chunk's first key of that bucket.  The chunk's flags (0 empty,
+// 1 one value, 2 several) and values go to global memory for segment_emit.
+constexpr int kSThreads = 512;
+constexpr int kSWarps = kSThreads / 32;      // 16
+constexpr int kSItems = 16;                  // keys per thread per tile
+constexpr int kSTile = kSThreads * kSItems;  // 8192
+constexpr int kSPairs = kSWarps / 2;         // counter words per bucket (two warps per word)
+constexpr int kSBpt = kMaxK / kSThreads;     // buckets per thread (t and t + 512)
+static_assert(kSBpt == 2, "bucket ownership t, t + kSThreads");
 
-__host__ __device__ constexpr size_t scatter_smem_bytes(uint32_t k) {
-  return (size_t)kSTile4 * 8 + (size_t)k * 8 * 3 + (size_t)kSTile4 * 4 +
-         (size_t)kSPairs4 * k * 4 + (size_t)(k + 1) * 4 + (size_t)k + 16;
+__host__ __device__ constexpr size_t scatter_stable_smem_bytes(uint32_t k) {
+  return (size_t)kSTile * 8 + (size_t)kSTile * 2 + (size_t)2 * kSPairs * k * 4 + (size_t)k * 8 +
+         (size_t)k * 4 * 2 + (size_t)k * 2 + 64;
 }
 
-template <bool F64, int MODE>
-__device__ void scatter_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_user,
-                              uint64_t* __restrict__ dst_scr, uint32_t c, const ChunkDesc& ch,
-                              const ModelDev& md, unsigned char* smraw) {
-  constexpr int NT = kSThreads4;
-  const uint32_t k = a.k;
-  uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);         // kSTile4
-  uint32_t* wc = reinterpret_cast<uint32_t*>(stage + kSTile4);   // kSPairs4 * k (16-B multiple)
-  uint64_t* runa = reinterpret_cast<uint64_t*>(wc + kSPairs4 * k);  // k: byte address of next write
-  uint64_t* ref = runa + k;                                      // k: chunk's first key
-  uint64_t* adj = ref + k;                                       // k: runa - 8 * tile offset
-  uint32_t* sbi = reinterpret_cast<uint32_t*>(adj + k);          // kSTile4: bucket << 16 | index
-  uint32_t* toff = sbi + kSTile4;                                // k + 1
-  uint8_t* cflag = reinterpret_cast<uint8_t*>(toff + k + 1);     // k
-  __shared__ uint32_t s_warp[40];
-  const Bucketer<F64, MODE> bucket(md, k);
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  for (uint32_t b = threadIdx.x; b < k; b += NT) {
-    const uint64_t d = a.seg_dst[(size_t)ch.seg * k + b] + a.chunk_pre[(size_t)c * k + b];
-    uint64_t* buf = (d & kDstUserBit) ? dst_user : dst_scr;
-    runa[b] = reinterpret_cast<uint64_t>(buf + (d & ~kDstUserBit));
-    cflag[b] = 0;
-  }
-  uint32_t* wcw = wc + (wp >> 1) * k;
-  const uint32_t winc = 1u << (16 * (wp & 1));
-  const int wsh = 16 * (wp & 1);
-  const uint64_t* p = a.src + ch.start;
-  uint64_t key[kSRounds4];
-#pragma unroll
-  for (int r = 0; r < kSRounds4; ++r) {
-    const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
-    key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
-  }
 #ifdef IPLS_SCATTER_TIMING
-  long long t_prev_ = clock64();
 #define SC_TICK(N) do { if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_sc_phase[N], (unsigned long long)(t_ - t_prev_)); t_prev_ = t_; } } while (0)
 #else
 #define SC_TICK(N)
 #endif
+
+__device__ int g_force_match_rank;  // ipls_debug_force_match_rank: every CTA ranks by match.any
+
+// L2 evict_last policy for the run stores (created once per thread)
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_hint(uint64_t* p, uint64_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Warp 0: are same-address lanes of one shared-memory atomicAdd served in lane order?  Four
+// lane patterns (all lanes on one word; two interleaved groups; blocks of 8; a scrambled
+// 4-group pattern), each compared with the rank popc(lanes below on the same word).
+__device__ bool atomic_lane_order_ok(uint32_t* scratch /* 4 words */) {
+  const uint32_t lane = threadIdx.x & 31;
+  bool ok = true;
+#pragma unroll
+  for (int pat = 0; pat < 4; ++pat) {
+    auto addr = [&](uint32_t l) -> uint32_t {
+      return pat == 0 ? 0u : pat == 1 ? (l & 1u) : pat == 2 ? (l >> 3) : ((l * 13u + 5u) >> 2) & 3u;
+    };
+    if (lane < 4) scratch[lane] = 0u;
+    __syncwarp();
+    const uint32_t my = addr(lane);
+    const uint32_t got = atomicAdd(&scratch[my], 1u);
+    uint32_t want = 0;
+    for (uint32_t l = 0; l < lane; ++l) want += addr(l) == my ? 1u : 0u;
+    ok &= got == want;
+    __syncwarp();
+  }
+  return __all_sync(0xffffffffu, ok);
+}
+
+// Destination of a chunk's bucket runs: the buffer and every run's absolute start (u32; the
+// ABI limits n to 2^32 - 1 keys).
+template <int NT>
+__device__ __forceinline__ uint64_t* chunk_runs(const LevelArgs& a, uint64_t* dst_user,
+                                                uint64_t* dst_scr, uint32_t c, uint32_t seg,
+                                                uint32_t* runo) {
+  const uint32_t k = a.k;
+  for (uint32_t b = threadIdx.x; b < k; b += NT) {
+    const uint64_t d = a.seg_dst[(size_t)seg * k + b] + a.chunk_pre[(size_t)c * k + b];
+    runo[b] = (uint32_t)(d & ~kDstUserBit);
+  }
+  return (a.seg_dst[(size_t)seg * k] & kDstUserBit) ? dst_user : dst_scr;
+}
+
+// Exclusive scan of one u32 per thread over the CTA with one barrier (the warp totals are
+// read by every thread; `sw` must not be reused before the caller's next barrier).
+template <int NT>
+__device__ __forceinline__ uint32_t scan_excl_1bar(uint32_t x, uint32_t* sw, uint32_t& total) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) sw[w] = inc;
+  __syncthreads();
+  // every warp scans the NW warp totals itself (one load per lane, shuffles): no second
+  // barrier, and no NW broadcast loads per thread
+  const uint32_t wt = (lane < NW) ? sw[lane] : 0u;
+  uint32_t wi = wt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+    if (lane >= o) wi += y;
+  }
+  const uint32_t before = __shfl_sync(0xffffffffu, wi - wt, w);
+  total = __shfl_sync(0xffffffffu, wi, NW - 1);
+  return before + inc - x;
+}
+
+// Rank modes of phase A in the stable kernel.
+constexpr int kRankAtomic = 0, kRankDense = 1, kRankMatch = 2;
+
+template <bool F64, int MODE>
+__device__ void scatter_stable_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_user,
+                                     uint64_t* __restrict__ dst_scr, uint32_t c,
+                                     const ChunkDesc& ch, const ModelDev& md,
+                                     unsigned char* smraw) {
+  constexpr int NT = kSThreads;
+  constexpr bool kStageBucket = MODE == (int)kModelTree;  // a tree descent costs more than a load
+  const uint32_t k = a.k;
+  uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);              // kSTile keys
+  uint16_t* sbk = reinterpret_cast<uint16_t*>(stage + kSTile);        // kSTile (tree only)
+  uint32_t* tab0 = reinterpret_cast<uint32_t*>(sbk + kSTile);         // 2 x kSPairs x k counters
+  uint64_t* ref = reinterpret_cast<uint64_t*>(tab0 + 2 * kSPairs * k);  // k: chunk's first key
+  uint32_t* runo = reinterpret_cast<uint32_t*>(ref + k);              // k: next write position
+  uint32_t* adjo = runo + k;                                          // k: runo - run start
+  uint8_t* seen = reinterpret_cast<uint8_t*>(adjo + k);               // k: bucket seen in chunk
+  uint8_t* multi = seen + k;                                          // k: several values seen
+  __shared__ uint32_t s_warp[2][kSWarps];
+  __shared__ uint32_t s_probe[4];
+  __shared__ int s_match;
+  const Bucketer<F64, MODE> bucket(md, k);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const uint32_t t = threadIdx.x;
+  const uint32_t lt = lanemask_lt();
+  uint64_t* dst = chunk_runs<NT>(a, dst_user, dst_scr, c, ch.seg, runo);
+  for (uint32_t b = t; b < k; b += NT) { seen[b] = 0; multi[b] = 0; }
+  {  // both counter tables start cleared
+    uint4* z = reinterpret_cast<uint4*>(tab0);
+    for (uint32_t i = t; i < 2 * kSPairs * k / 4; i += NT) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  if (wp == 0) {
+    const bool ok = atomic_lane_order_ok(s_probe);
+    if (lane == 0) s_match = (!ok || *((volatile int*)&g_force_match_rank)) ? 1 : 0;
+  }
+  const uint64_t pol = policy_evict_last();
+  const uint32_t winc = 1u << (16 * (wp & 1));
+  const int wsh = 16 * (wp & 1);
+  const uint64_t* p = a.src + ch.start;
+  uint64_t key[kSItems];
+#pragma unroll
+  for (int r = 0; r < kSItems; ++r) {
+    const uint32_t i = wp * (kSItems * 32) + r * 32 + lane;
+    key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
+  }
+  __syncthreads();
+  const bool use_match = s_match != 0;  // block-uniform
+#ifdef IPLS_SCATTER_TIMING
+  long long t_prev_ = clock64();
+#endif
   bool dense = false;  // block-uniform
-  for (uint32_t t0 = 0; t0 < ch.len; t0 += kSTile4) {
-    const uint32_t tl = min((uint32_t)kSTile4, ch.len - t0);
-    {
-      uint4* w4 = reinterpret_cast<uint4*>(wc);
-      for (uint32_t i = threadIdx.x; i < kSPairs4 * k / 4; i += NT) w4[i] = make_uint4(0, 0, 0, 0);
+  int it = 0;
+  for (uint32_t t0 = 0; t0 < ch.len; t0 += kSTile, ++it) {
+    const uint32_t tl = min((uint32_t)kSTile, ch.len - t0);
+    const bool full = tl == (uint32_t)kSTile;  // block-uniform: no bounds checks
+    uint32_t* tab = tab0 + (it & 1) * (kSPairs * k);
+    uint32_t* tabn = tab0 + ((it & 1) ^ 1) * (kSPairs * k);
+    uint32_t* tw = tab + (wp >> 1) * k;
+    // ---- (A) ranks: bucket | in-warp rank << 16 ----
+    uint32_t bl[kSItems];
+    if (full && !dense && !use_match) {
+      // all buckets, then all atomics back to back, then the ranks: the atomics' latency
+      // overlaps instead of stalling every item
+#pragma unroll
+      for (int r = 0; r < kSItems; ++r) bl[r] = bucket(key[r]);
+      uint32_t old[kSItems];
+#pragma unroll
+      for (int r = 0; r < kSItems; ++r) old[r] = atomicAdd(&tw[bl[r]], winc);
+#pragma unroll
+      for (int r = 0; r < kSItems; ++r) bl[r] |= ((old[r] >> wsh) & 0xffffu) << 16;
+    } else {
+      auto rank_items = [&](auto mode_tag) {
+        constexpr int RM = decltype(mode_tag)::value;
+#pragma unroll
+        for (int r = 0; r < kSItems; ++r) {
+          const uint32_t i = wp * (kSItems * 32) + r * 32 + lane;
+          const bool valid = i < tl;
+          const uint32_t b = valid ? bucket(key[r]) : 0u;
+          uint32_t loc = 0;
+          if constexpr (RM == kRankMatch) {
+            const uint32_t peers = __match_any_sync(0xffffffffu, valid ? b : 0xffffffffu);
+            const int leader = __ffs(peers) - 1;
+            uint32_t old = 0;
+            if (valid && lane == leader) old = atomicAdd(&tw[b], __popc(peers) * winc);
+            old = __shfl_sync(0xffffffffu, old, leader);
+            loc = ((old >> wsh) & 0xffffu) + __popc(peers & lt);
+          } else if constexpr (RM == kRankDense) {
+            // few buckets per tile (presorted, clustered or EQ3 input): a warp whose keys
+            // share one bucket takes one atomic instead of 32 serialised same-address lanes
+            const uint32_t b0 = __shfl_sync(0xffffffffu, b, 0);
+            if (__all_sync(0xffffffffu, !valid || b == b0)) {
+              const uint32_t nv = __popc(__ballot_sync(0xffffffffu, valid));
+              uint32_t base = 0;
+              if (lane == 0 && nv) base = atomicAdd(&tw[b0], nv * winc);
+              loc = ((__shfl_sync(0xffffffffu, base, 0) >> wsh) & 0xffffu) + lane;
+            } else if (valid) {
+              loc = (atomicAdd(&tw[b], winc) >> wsh) & 0xffffu;
+            }
+          } else {
+            if (valid) loc = (atomicAdd(&tw[b], winc) >> wsh) & 0xffffu;
+          }
+          bl[r] = b | (loc << 16);
+        }
+      };
+      if (use_match) rank_items(std::integral_constant<int, kRankMatch>{});
+      else if (dense) rank_items(std::integral_constant<int, kRankDense>{});
+      else rank_items(std::integral_constant<int, kRankAtomic>{});
     }
     __syncthreads();
     SC_TICK(0);
-    uint32_t bl[kSRounds4];  // bucket | in-warp rank << 16
-    if (dense) {
-      // Few buckets per tile (presorted, clustered or EQ3 input): a warp whose keys share one
-      // bucket takes one atomic for all of them instead of 32 serialised same-address atomics.
+#ifdef IPLS_SCATTER_TIMING
+    if (threadIdx.x == 0) atomicAdd(&g_sc_phase[28], 1ull);
+#endif
+    // ---- (B) warp prefixes and run starts per bucket ----
+    uint32_t cnt[kSBpt], wv[kSBpt][kSPairs];
 #pragma unroll
-      for (int r = 0; r < kSRounds4; ++r) {
-        const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
-        const bool valid = i < tl;
-        const uint32_t b = valid ? bucket(key[r]) : 0u;
-        const uint32_t b0 = __shfl_sync(0xffffffffu, b, 0);
-        bl[r] = 0;
-        if (__all_sync(0xffffffffu, !valid || b == b0)) {
-          const uint32_t nv = __popc(__ballot_sync(0xffffffffu, valid));
-          uint32_t base = 0;
-          if (lane == 0 && nv) base = atomicAdd(&wcw[b0], nv * winc);
-          base = (__shfl_sync(0xffffffffu, base, 0) >> wsh) & 0xffffu;
-          if (valid) bl[r] = b | ((base + lane) << 16);
-        } else if (valid) {
-          const uint32_t loc = (atomicAdd(&wcw[b], winc) >> wsh) & 0xffffu;
-          bl[r] = b | (loc << 16);
+    for (int q = 0; q < kSBpt; ++q) {
+      const uint32_t b = t + q * NT;
+      uint32_t s = 0;
+#pragma unroll
+      for (int pp = 0; pp < kSPairs; ++pp) {
+        wv[q][pp] = (b < k) ? tab[pp * k + b] : 0u;
+        s += wv[q][pp];
+      }
+      cnt[q] = (s & 0xffffu) + (s >> 16);  // no carry: a tile holds <= 8192 keys
+    }
+    {  // clear the other table for the next tile
+      uint4* z = reinterpret_cast<uint4*>(tabn);
+#pragma unroll
+      for (int j = 0; j < kSPairs * kMaxK / 4 / NT; ++j) {
+        const uint32_t i = t + j * NT;
+        if (i < kSPairs * k / 4) z[i] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    uint32_t tot;
+    const uint32_t ex = scan_excl_1bar<NT>(cnt[0] | (cnt[1] << 16), s_warp[it & 1], tot);
+    const uint32_t off[kSBpt] = {ex & 0xffffu, (tot & 0xffffu) + (ex >> 16)};
+#pragma unroll
+    for (int q = 0; q < kSBpt; ++q) {
+      const uint32_t b = t + q * NT;
+      if (b < k) {
+        const uint32_t ro = runo[b];
+        adjo[b] = ro - off[q];
+        runo[b] = ro + cnt[q];
+        uint32_t run = off[q];
+#pragma unroll
+        for (int pp = 0; pp < kSPairs; ++pp) {
+          const uint32_t w = wv[q][pp], lo = w & 0xffffu;
+          tab[pp * k + b] = run | ((run + lo) << 16);
+          run += lo + (w >> 16);
         }
+      }
+    }
+    // next tile's path: dense when this tile averages >= 32 keys per non-empty bucket
+    // (__syncthreads_count counts threads: bucket t + 512 is assumed as full as bucket t)
+    dense = (uint32_t)__syncthreads_count(cnt[0] != 0) * (k > NT ? 2u : 1u) * 32u <= tl;
+    SC_TICK(1);
+    // ---- (C) placement into the stage; loads of the next tile ----
+    if (full) {
+      uint32_t pos[kSItems];
+#pragma unroll
+      for (int r = 0; r < kSItems; ++r) pos[r] = tw[bl[r] & 0xffffu];
+#pragma unroll
+      for (int r = 0; r < kSItems; ++r) {
+        const uint32_t q = ((pos[r] >> wsh) & 0xffffu) + (bl[r] >> 16);
+        stage[q] = key[r];
+        if constexpr (kStageBucket) sbk[q] = (uint16_t)(bl[r] & 0xffffu);
       }
     } else {
 #pragma unroll
-      for (int r = 0; r < kSRounds4; ++r) {
-        const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
-        bl[r] = 0;
+      for (int r = 0; r < kSItems; ++r) {
+        const uint32_t i = wp * (kSItems * 32) + r * 32 + lane;
         if (i < tl) {
-          const uint32_t b = bucket(key[r]);
-          const uint32_t loc = (atomicAdd(&wcw[b], winc) >> wsh) & 0xffffu;
-          bl[r] = b | (loc << 16);
+          const uint32_t b = bl[r] & 0xffffu;
+          const uint32_t q = ((tw[b] >> wsh) & 0xffffu) + (bl[r] >> 16);
+          stage[q] = key[r];
+          if constexpr (kStageBucket) sbk[q] = (uint16_t)b;
         }
       }
     }
-    __syncthreads();
-    SC_TICK(1);
-    // Per bucket: tile count (sum over the warps), scan over buckets, then every warp's word
-    // becomes the absolute staged position of its first key of the bucket (tile offset +
-    // exclusive prefix over the earlier warps: warp order = key order).
-    uint32_t cnt[kSBpt], csum = 0;
 #pragma unroll
-    for (int q = 0; q < kSBpt; ++q) {
-      const uint32_t b = threadIdx.x * kSBpt + q;
-      uint32_t run = 0;
-      if (b < k) {
-#pragma unroll
-        for (int w2 = 0; w2 < kSPairs4; ++w2) {
-          const uint32_t wv = wc[w2 * k + b];
-          run += (wv & 0xffffu) + (wv >> 16);
-        }
-      }
-      cnt[q] = run;
-      csum += run;
-    }
-    {
-      uint32_t ex = block_exclusive_scan<NT>(csum, s_warp, nullptr);
-#pragma unroll
-      for (int q = 0; q < kSBpt; ++q) {
-        const uint32_t b = threadIdx.x * kSBpt + q;
-        if (b < k) {
-          toff[b] = ex;
-          adj[b] = runa[b] - 8ull * ex;
-          uint32_t run = ex;
-#pragma unroll
-          for (int w2 = 0; w2 < kSPairs4; ++w2) {
-            const uint32_t wv = wc[w2 * k + b];
-            const uint32_t lo = wv & 0xffffu, hi = wv >> 16;
-            wc[w2 * k + b] = run | ((run + lo) << 16);
-            run += lo + hi;
-          }
-        }
-        ex += cnt[q];
-      }
-      if (threadIdx.x == NT - 1) toff[k] = ex;
-    }
-    static_assert(kSBpt == 1, "one bucket per thread in the tile statistics");
-    // next tile's path: dense when the tile's keys average >= 32 per non-empty bucket
-    dense = __syncthreads_count(cnt[0] != 0) * 32u <= tl;
-    SC_TICK(2);
-#pragma unroll
-    for (int r = 0; r < kSRounds4; ++r) {
-      const uint32_t i = wp * (kSRounds4 * 32) + r * 32 + lane;
-      if (i < tl) {
-        const uint32_t b = bl[r] & 0xffffu;
-        const uint32_t pos = ((wcw[b] >> wsh) & 0xffffu) + (bl[r] >> 16);
-        stage[pos] = key[r];
-        sbi[pos] = (b << 16) | i;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < kSRounds4; ++r) {  // prefetch the next tile while this one drains
-      const uint32_t i = t0 + kSTile4 + wp * (kSRounds4 * 32) + r * 32 + lane;
+    for (int r = 0; r < kSItems; ++r) {
+      const uint32_t i = t0 + kSTile + wp * (kSItems * 32) + r * 32 + lane;
       key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
     }
-    {  // and the tile after it into the L2, one 128-byte line per thread (C5 -1.3 %)
-      const uint32_t i = t0 + 2 * kSTile4 + threadIdx.x * 16;
-      if (threadIdx.x < kSTile4 / 16 && i < ch.len)
-        asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(p + i));
+    {  // and the tile after it into the L2, one 128-byte line per thread
+      const uint32_t i = t0 + 2 * kSTile + t * 16;
+      if (i < ch.len) asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(p + i));
     }
     __syncthreads();
-    SC_TICK(3);
-    // Write-out: staged key q goes to adj[bucket] + 8 q.  Its staged predecessor decides the
-    // stability check (same bucket => increasing tile index) and the in-tile homogeneity check
-    // (same bucket => same value); both are sequential smem reads.
-    int bad = 0;
-    for (uint32_t q = threadIdx.x; q < tl; q += NT) {
-      const uint32_t x = sbi[q];
-      const uint32_t b = x >> 16;
-      const uint64_t v = stage[q];
-      if (q > 0) {
-        const uint32_t y = sbi[q - 1];
-        if ((y >> 16) == b) {
-          if ((y & 0xffffu) > (x & 0xffffu)) bad = 1;
-          if (stage[q - 1] != v) cflag[b] = 2;
-        }
+    SC_TICK(2);
+    // ---- (D) write-out: warp w writes staged slots [512 w, 512 w + 512), 8 at a time ----
+    {
+      const uint32_t q0 = wp * (kSItems * 32);
+      // the staged predecessor of slot q comes from lane - 1 (a rotate by one lane); lane 0
+      // takes lane 31's from the previous batch item
+      uint64_t cv = 0;
+      uint32_t cb = 0xffffffffu;  // no predecessor
+      if (q0 > 0 && q0 - 1 < tl) {
+        cv = stage[q0 - 1];
+        if constexpr (kStageBucket) cb = sbk[q0 - 1]; else cb = bucket(cv);
       }
-      st_evict_last(reinterpret_cast<uint64_t*>(adj[b]) + q, v);
-    }
-    SC_TICK(4);
-    if (__syncthreads_or(bad)) {
-      // Repair (never observed on B200): rewrite every bucket run in tile-index order.
-      for (uint32_t b = threadIdx.x; b < k; b += NT) {
-        const uint32_t beg = toff[b], end = toff[b + 1];
-        for (uint32_t i = beg + 1; i < end; ++i) {
-          const uint32_t xi = sbi[i];
-          const uint64_t xv = stage[i];
-          uint32_t j = i;
-          while (j > beg && (sbi[j - 1] & 0xffffu) > (xi & 0xffffu)) {
-            sbi[j] = sbi[j - 1];
-            stage[j] = stage[j - 1];
-            --j;
-          }
-          sbi[j] = xi;
-          stage[j] = xv;
-        }
-        for (uint32_t q = beg; q < end; ++q) reinterpret_cast<uint64_t*>(runa[b])[q - beg] = stage[q];
-      }
-      __syncthreads();
-    }
-    SC_TICK(5);
+      const int src_lane = (lane + 31) & 31;
 #pragma unroll
-    for (int q = 0; q < kSBpt; ++q) {
-      const uint32_t b = threadIdx.x * kSBpt + q;
-      if (b < k && cnt[q]) {
-        const uint64_t f = stage[toff[b]];
-        const uint8_t cf = cflag[b];
-        if (cf == 0) { ref[b] = f; cflag[b] = 1; }
-        else if (cf == 1 && ref[b] != f) cflag[b] = 2;
-        runa[b] += 8ull * cnt[q];
+      for (int h = 0; h < kSItems / 8; ++h) {
+        uint64_t v[8];
+        uint32_t b[8], ao[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t q = q0 + (h * 8 + j) * 32 + lane;
+          v[j] = (full || q < tl) ? stage[q] : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t q = q0 + (h * 8 + j) * 32 + lane;
+          if constexpr (kStageBucket) b[j] = (full || q < tl) ? sbk[q] : 0xfffffffeu;
+          else b[j] = (full || q < tl) ? bucket(v[j]) : 0xfffffffeu;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ao[j] = adjo[min(b[j], k - 1)];  // invalid slots: any bucket
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t q = q0 + (h * 8 + j) * 32 + lane;
+          const uint64_t rv = __shfl_sync(0xffffffffu, v[j], src_lane);
+          const uint32_t rb = __shfl_sync(0xffffffffu, b[j], src_lane);
+          const uint64_t vp = lane ? rv : cv;
+          const uint32_t bp = lane ? rb : cb;
+          cv = rv;
+          cb = rb;
+          if (full || q < tl) {
+            if (b[j] == bp) {
+              if (v[j] != vp) multi[b[j]] = 1;
+            } else {  // first key of bucket b's run in this tile
+              if (!seen[b[j]]) { ref[b[j]] = v[j]; seen[b[j]] = 1; }
+              else if (ref[b[j]] != v[j]) multi[b[j]] = 1;
+            }
+            st_hint(dst + (uint32_t)(ao[j] + q), v[j], pol);
+          }
+        }
       }
     }
-    SC_TICK(6);
+    SC_TICK(3);
   }
   __syncthreads();
-  for (uint32_t b = threadIdx.x; b < k; b += NT) {
-    const uint8_t cf = cflag[b];
+  for (uint32_t b = t; b < k; b += NT) {
+    const uint8_t cf = seen[b] ? (multi[b] ? 2 : 1) : 0;
     a.cflag[(size_t)c * k + b] = cf;
     if (cf == 1) a.cref[(size_t)c * k + b] = ref[b];
   }
 }
 
+// Terminal chunks (k_scatter_term): 1024 threads (32 warps, 1 CTA per SM), tiles of 8192 keys
+// streamed through a ring of kTRing smem slots by TMA bulk copies issued two tiles ahead, so
+// no load latency is exposed inside a chunk and keys never wait in prefetch registers.  A
+// slot doubles as its tile's stage: (A) keys to registers + count per bucket, (B) run starts,
+// (C) placement by an atomic cursor per bucket into the same slot, (D) write-out with the
+// bucket recomputed from the staged key.  No warp counters, no homogeneity (terminal
+// segments have no child above the base case).
+constexpr int kTThreads = 1024;
+constexpr int kTItems = 8;
+constexpr int kTTile = kTThreads * kTItems;   // 8192
+constexpr int kTRing = 3;
+constexpr int kTSlot = kTTile + 4;            // keys per slot (+ parity shift, 32-byte multiple)
 
-// Terminal segments (every child <= base case): the children are sorted by the base case
-// right after this level, so the scatter does not need stable ranks.  Per tile: bucket counts
-// (smem atomics), a scan over buckets, placement by an atomic cursor per bucket, write-out as
-// in the stable path (the staged key's bucket is recomputed there rather than staged).  No per-warp counters, no cross-warp scan, no stability check; no
-// homogeneity tracking either (only children above the base case can be homogeneous-final).
-// Tiles are twice as long as the stable path's (16 keys per thread): half the barriers and
-// scans per key, and bucket runs twice as long per tile (fuller L2 lines per write-out).
-#ifndef IPLS_UROUNDS
-#define IPLS_UROUNDS 16
-#endif
-constexpr int kURounds = IPLS_UROUNDS;             // keys per thread per tile
-constexpr int kUTile = kSThreads4 * kURounds;      // 16384
-__host__ __device__ constexpr size_t scatter_unstable_smem_bytes(uint32_t k) {
-  return (size_t)kUTile * 8 + (size_t)k * 8 * 2 + (size_t)k * 4 * 2 + (size_t)kUTile * 2;
+__host__ __device__ constexpr size_t scatter_term_smem_bytes(uint32_t k) {
+  return (size_t)kTRing * kTSlot * 8 + (size_t)k * 4 * 4 + 64;
+}
+
+// Tile [t0, t0 + tl) of a chunk starting at p (h = parity of its start): the keys land at
+// slot[h + i].  One TMA bulk copy completing on `bar` moves the 16-byte-aligned span around
+// them (a key before and after the tile are read along and ignored); only at the very end of
+// the array, where no key follows an odd span, the last key is loaded by the issuing thread
+// itself (synchronously: once per level).  Thread 0 only.  room = keys from p + t0 to the end
+// of the array.
+__device__ __forceinline__ void tile_issue(uint64_t* slot, const uint64_t* p, uint32_t h,
+                                           uint32_t t0, uint32_t tl, uint64_t room, uint64_t* bar) {
+  uint32_t n = h + tl;               // keys from p + t0 - h (16-byte aligned)
+  if ((n & 1u) && (uint64_t)tl < room) ++n;
+  const uint32_t body = n & ~1u;
+  if (n & 1u) slot[n - 1] = __ldcs(p + t0 + tl - 1);
+  if (body) {
+    mbar_arrive_tx(bar, body * 8u);
+    bulk_g2s(slot, p + t0 - h, body * 8u, bar);
+  } else {
+    mbar_arrive(bar);
+  }
 }
 
 template <bool F64, int MODE>
-__device__ void scatter_chunk_unstable(const LevelArgs& a, uint64_t* __restrict__ dst_user,
-                                       uint64_t* __restrict__ dst_scr, uint32_t c,
-                                       const ChunkDesc& ch, const ModelDev& md,
-                                       unsigned char* smraw) {
-  constexpr int NT = kSThreads4;
+__device__ void scatter_term_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_user,
+                                   uint64_t* __restrict__ dst_scr, uint32_t c,
+                                   const ChunkDesc& ch, const ModelDev& md, unsigned char* smraw) {
+  constexpr int NT = kTThreads;
   const uint32_t k = a.k;
-  uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);          // kUTile
-  uint64_t* runa = stage + kUTile;                                // k
-  uint64_t* adj = runa + k;                                       // k
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(adj + k);           // k
-  uint32_t* cur = cnt + k;                                        // k
-  uint16_t* sbk = reinterpret_cast<uint16_t*>(cur + k);           // kUTile (tree only)
-  __shared__ uint32_t s_warp[40];
+  uint64_t* slots = reinterpret_cast<uint64_t*>(smraw);            // kTRing x kTSlot
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(slots + kTRing * kTSlot);  // k
+  uint32_t* cur = cnt + k;                                          // k: placement cursor
+  uint32_t* runo = cur + k;                                         // k
+  uint32_t* adjo = runo + k;                                        // k
+  __shared__ uint32_t s_warp[2][32];
+  __shared__ __align__(8) uint64_t s_bar[kTRing];
   const Bucketer<F64, MODE> bucket(md, k);
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  for (uint32_t b = threadIdx.x; b < k; b += NT) {
-    const uint64_t d = a.seg_dst[(size_t)ch.seg * k + b] + a.chunk_pre[(size_t)c * k + b];
-    uint64_t* buf = (d & kDstUserBit) ? dst_user : dst_scr;
-    runa[b] = reinterpret_cast<uint64_t>(buf + (d & ~kDstUserBit));
-  }
+  const int lane = threadIdx.x & 31;
+  const uint32_t t = threadIdx.x;
+  uint64_t* dst = chunk_runs<NT>(a, dst_user, dst_scr, c, ch.seg, runo);
+  for (uint32_t b = t; b < k; b += NT) cnt[b] = 0;
   const uint64_t* p = a.src + ch.start;
-  uint64_t key[kURounds];
+  const uint32_t h = (uint32_t)(reinterpret_cast<uintptr_t>(p) >> 3) & 1u;
+  const uint32_t ntile = (ch.len + kTTile - 1) / kTTile;
+  const uint64_t room = a.nkeys - ch.start;
+  if (t == 0) {
 #pragma unroll
-  for (int r = 0; r < kURounds; ++r) {
-    const uint32_t i = wp * (kURounds * 32) + r * 32 + lane;
-    key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
+    for (int s = 0; s < kTRing; ++s) mbar_init(&s_bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (uint32_t j = 0; j < min(ntile, (uint32_t)kTRing - 1); ++j)
+      tile_issue(slots + j * kTSlot, p, h, j * kTTile, min((uint32_t)kTTile, ch.len - j * kTTile),
+                 room - j * kTTile, &s_bar[j]);
   }
+  const uint64_t pol = policy_evict_last();
+  __syncthreads();
 #ifdef IPLS_SCATTER_TIMING
   long long t_prev_ = clock64();
 #endif
   bool dense = false;  // block-uniform
-  for (uint32_t t0 = 0; t0 < ch.len; t0 += kUTile) {
-    const uint32_t tl = min((uint32_t)kUTile, ch.len - t0);
-    for (uint32_t b = threadIdx.x; b < k; b += NT) cnt[b] = 0u;
-    __syncthreads();
-#ifdef IPLS_SCATTER_TIMING
-    if (threadIdx.x == 0) atomicAdd(&g_sc_phase[15], 1ull);
-#endif
-    SC_TICK(11);
-    uint32_t bk[kURounds / 2];  // two buckets per word; 0xffff = no key
+  for (uint32_t it = 0; it < ntile; ++it) {
+    const uint32_t t0 = it * kTTile;
+    const uint32_t tl = min((uint32_t)kTTile, ch.len - t0);
+    const uint32_t s = it % kTRing;
+    uint64_t* slot = slots + s * kTSlot;
+    mbar_wait(&s_bar[s], (it / kTRing) & 1u);
+    // ---- (A) keys to registers, counts ----
+    uint64_t v[kTItems];
+    uint32_t bk[kTItems];
 #pragma unroll
-    for (int r = 0; r < kURounds; ++r) {
-      const uint32_t i = wp * (kURounds * 32) + r * 32 + lane;
-      uint32_t bb = 0xffffu;
-      if (i < tl) bb = bucket(key[r]);
-      if (dense) {  // as in the stable path: one atomic for a warp of one bucket
-        const uint32_t b0 = __shfl_sync(0xffffffffu, bb, 0);
-        if (__all_sync(0xffffffffu, bb == 0xffffu || bb == b0)) {
-          const uint32_t nv = __popc(__ballot_sync(0xffffffffu, bb != 0xffffu));
+    for (int r = 0; r < kTItems; ++r) {
+      const uint32_t i = r * NT + t;
+      v[r] = (i < tl) ? slot[h + i] : 0ull;
+      bk[r] = (i < tl) ? bucket(v[r]) : 0xffffffffu;
+    }
+    if (!dense) {
+#pragma unroll
+      for (int r = 0; r < kTItems; ++r)
+        if (bk[r] != 0xffffffffu) atomicAdd(&cnt[bk[r]], 1u);
+    } else {
+#pragma unroll
+      for (int r = 0; r < kTItems; ++r) {
+        const uint32_t b0 = __shfl_sync(0xffffffffu, bk[r], 0);
+        if (__all_sync(0xffffffffu, bk[r] == b0 || bk[r] == 0xffffffffu)) {
+          const uint32_t nv = __popc(__ballot_sync(0xffffffffu, bk[r] != 0xffffffffu));
           if (lane == 0 && nv) atomicAdd(&cnt[b0], nv);
-        } else if (bb != 0xffffu) {
-          atomicAdd(&cnt[bb], 1u);
+        } else if (bk[r] != 0xffffffffu) {
+          atomicAdd(&cnt[bk[r]], 1u);
         }
-      } else if (bb != 0xffffu) {
-        atomicAdd(&cnt[bb], 1u);
       }
-      if (r & 1) bk[r >> 1] |= bb << 16;
-      else bk[r >> 1] = bb;
     }
     __syncthreads();
-    SC_TICK(12);
-    {
-      uint32_t cc[kSBpt], sum = 0;
+    SC_TICK(4);
+#ifdef IPLS_SCATTER_TIMING
+    if (threadIdx.x == 0) atomicAdd(&g_sc_phase[29], 1ull);
+#endif
+    // every thread is past D(it - 1): its slot takes tile it + kTRing - 1
+    if (t == 0 && it + kTRing - 1 < ntile) {
+      const uint32_t jn = it + kTRing - 1, sn = jn % kTRing;
+      tile_issue(slots + sn * kTSlot, p, h, jn * kTTile, min((uint32_t)kTTile, ch.len - jn * kTTile),
+                 room - jn * kTTile, &s_bar[sn]);
+    }
+    // ---- (B) run starts (scan over buckets, thread t owns bucket t) ----
+    uint32_t cc = 0;
+    if (t < k) { cc = cnt[t]; cnt[t] = 0; }
+    uint32_t tot;
+    const uint32_t off = scan_excl_1bar<NT>(cc, s_warp[it & 1], tot);
+    if (t < k) {
+      cur[t] = off;
+      const uint32_t ro = runo[t];
+      adjo[t] = ro - off;
+      runo[t] = ro + cc;
+    }
+    dense = (uint32_t)__syncthreads_count(cc != 0) * 32u <= tl;
+    SC_TICK(5);
+    // ---- (C) placement into the slot (every thread holds its keys in registers) ----
+    if (!dense) {
 #pragma unroll
-      for (int q = 0; q < kSBpt; ++q) {
-        const uint32_t b = threadIdx.x * kSBpt + q;
-        cc[q] = (b < k) ? cnt[b] : 0u;
-        sum += cc[q];
-      }
-      uint32_t ex = block_exclusive_scan<NT>(sum, s_warp, nullptr);
+      for (int r = 0; r < kTItems; ++r)
+        if (bk[r] != 0xffffffffu) bk[r] = atomicAdd(&cur[bk[r]], 1u);
+    } else {
 #pragma unroll
-      for (int q = 0; q < kSBpt; ++q) {
-        const uint32_t b = threadIdx.x * kSBpt + q;
-        if (b < k) {
-          cur[b] = ex;
-          const uint64_t ra = runa[b];
-          adj[b] = ra - 8ull * ex;
-          runa[b] = ra + 8ull * cc[q];
+      for (int r = 0; r < kTItems; ++r) {
+        const uint32_t b0 = __shfl_sync(0xffffffffu, bk[r], 0);
+        if (__all_sync(0xffffffffu, bk[r] == b0 || bk[r] == 0xffffffffu)) {
+          const uint32_t nv = __popc(__ballot_sync(0xffffffffu, bk[r] != 0xffffffffu));
+          uint32_t base = 0;
+          if (lane == 0 && nv) base = atomicAdd(&cur[b0], nv);
+          if (bk[r] != 0xffffffffu) bk[r] = __shfl_sync(0xffffffffu, base, 0) + lane;
+          else __shfl_sync(0xffffffffu, base, 0);
+        } else if (bk[r] != 0xffffffffu) {
+          bk[r] = atomicAdd(&cur[bk[r]], 1u);
         }
-        ex += cc[q];
-      }
-      dense = __syncthreads_count(cc[0] != 0) * 32u <= tl;  // this placement, next count
-    }
-    SC_TICK(13);
-#pragma unroll
-    for (int r = 0; r < kURounds; ++r) {
-      const uint32_t bb = (bk[r >> 1] >> (16 * (r & 1))) & 0xffffu;
-      const uint32_t b0 = dense ? __shfl_sync(0xffffffffu, bb, 0) : 0u;
-      if (dense && __all_sync(0xffffffffu, bb == 0xffffu || bb == b0)) {
-        const uint32_t nv = __popc(__ballot_sync(0xffffffffu, bb != 0xffffu));
-        uint32_t base = 0;
-        if (lane == 0 && nv) base = atomicAdd(&cur[b0], nv);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (bb != 0xffffu) {
-          stage[base + lane] = key[r];
-          if constexpr (MODE == (int)kModelTree) sbk[base + lane] = (uint16_t)bb;
-        }
-      } else if (bb != 0xffffu) {
-        const uint32_t pos = atomicAdd(&cur[bb], 1u);
-        stage[pos] = key[r];
-        if constexpr (MODE == (int)kModelTree) sbk[pos] = (uint16_t)bb;
       }
     }
 #pragma unroll
-    for (int r = 0; r < kURounds; ++r) {  // prefetch the next tile while this one drains
-      const uint32_t i = t0 + kUTile + wp * (kURounds * 32) + r * 32 + lane;
-      key[r] = (i < ch.len) ? __ldcs(p + i) : 0ull;
-    }
-    {  // and the tile after it into the L2, one 128-byte line per thread
-      const uint32_t i = t0 + 2 * kUTile + threadIdx.x * 16;
-      if (i < ch.len) asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(p + i));
-    }
+    for (int r = 0; r < kTItems; ++r)
+      if (r * NT + t < tl) slot[bk[r]] = v[r];
     __syncthreads();
-    SC_TICK(14);
-    // the bucket of a staged key is recomputed (same arithmetic, so the same bucket): cheaper
-    // than a random 2-byte smem store in the placement and a load here
-    for (uint32_t q = threadIdx.x; q < tl; q += NT) {
-      const uint64_t x = stage[q];
-      uint32_t b;
-      if constexpr (MODE == (int)kModelTree) b = sbk[q];  // a tree descent costs more
-      else b = bucket(x);
-      st_evict_last(reinterpret_cast<uint64_t*>(adj[b]) + q, x);
+    SC_TICK(6);
+    // ---- (D) write-out ----
+#pragma unroll
+    for (int r = 0; r < kTItems; ++r) {
+      const uint32_t q = r * NT + t;
+      v[r] = (q < tl) ? slot[q] : 0ull;
     }
-    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kTItems; ++r) bk[r] = adjo[bucket(v[r])];
+#pragma unroll
+    for (int r = 0; r < kTItems; ++r) {
+      const uint32_t q = r * NT + t;
+      if (q < tl) st_hint(dst + (uint32_t)(bk[r] + q), v[r], pol);
+    }
     SC_TICK(7);
   }
 }
 
-template <bool F64, bool TREE>
-__global__ __launch_bounds__(kSThreads4, 1) void k_scatter(LevelArgs a, uint64_t* __restrict__ dst_user,
-                                                           uint64_t* __restrict__ dst_scr) {
-  if (*((volatile const uint32_t*)a.err) & kErrNan) return;
+// After both scatter kernels: one CTA per segment classes its children (R20), applies the
+// no-progress guard (R10) and emits the next level's work, the base-case windows and the fills
+// (segment_emit).  A kernel of its own, so that the level's ~k-wide per-segment bookkeeping runs
+// on all SMs at once instead of as a serial tail inside the scatter CTA that finished last.
+constexpr int kEThreads = 512;
+__global__ __launch_bounds__(kEThreads) void k_emit(LevelArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ OffSmem os;
-  __shared__ uint32_t s_last;
-  const uint32_t c = blockIdx.x;
-  const ChunkDesc ch = a.chunks[c];
-  ModelDev md = a.models[ch.seg];
+  if (*((volatile const uint32_t*)a.err) & kErrNan) return;
+  const uint32_t s = blockIdx.x;
+  const SegDesc sg = a.segs[s];
+  const ModelDev md = a.models[s];
+  segment_emit<kEThreads>(a, s, sg, md, os, reinterpret_cast<uint32_t*>(smraw));
+}
+
+template <bool TREE, int NT>
+__device__ __forceinline__ void tree_top_to_smem(ModelDev& md, uint32_t k) {
   if constexpr (TREE) {  // top 8 levels of the splitter heap into smem
     __shared__ uint64_t s_top[256];
     if (md.kind == kModelTree)
-      for (uint32_t j = threadIdx.x; j < min(a.k, 256u); j += kSThreads4) s_top[j] = md.heap[j];
+      for (uint32_t j = threadIdx.x; j < min(k, 256u); j += NT) s_top[j] = md.heap[j];
     md.top = s_top;
     __syncthreads();
   }
-  const bool terminal = !a.single_offsets && a.seg_term[ch.seg];
+}
+
+template <bool F64, bool TREE>
+__global__ __launch_bounds__(kSThreads, 1) void k_scatter_stable(LevelArgs a, uint64_t* __restrict__ dst_user,
+                                                                 uint64_t* __restrict__ dst_scr) {
+  const uint32_t c = blockIdx.x;
+  const ChunkDesc ch = a.chunks[c];
+  if (!a.single_offsets && a.seg_term[ch.seg]) return;  // k_scatter_term's chunk
+  if (*((volatile const uint32_t*)a.err) & kErrNan) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  ModelDev md = a.models[ch.seg];
+  tree_top_to_smem<TREE, kSThreads>(md, a.k);
   constexpr int kMain = TREE ? (int)kModelTree : (int)kModelLinear;
-  if (terminal) {
-    if (md.kind == kModelEq3)
-      scatter_chunk_unstable<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw);
-    else
-      scatter_chunk_unstable<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
-  } else if (md.kind == kModelEq3) {
-    scatter_chunk<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw);
-  } else {
-    scatter_chunk<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
-  }
-  if (a.single_offsets) return;  // ipls_partition_level: no next level
-  const SegDesc sg = a.segs[ch.seg];
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&a.seg_done[ch.seg], 1u) == sg.nchunks - 1) ? 1u : 0u;
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    segment_emit<kSThreads4>(a, ch.seg, sg, md, os, reinterpret_cast<uint32_t*>(smraw));
-  }
+  if (md.kind == kModelEq3)
+    scatter_stable_chunk<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw);
+  else
+    scatter_stable_chunk<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
+}
+
+template <bool F64, bool TREE>
+__global__ __launch_bounds__(kTThreads, 1) void k_scatter_term(LevelArgs a, uint64_t* __restrict__ dst_user,
+                                                               uint64_t* __restrict__ dst_scr) {
+  const uint32_t c = blockIdx.x;
+  const ChunkDesc ch = a.chunks[c];
+  if (a.single_offsets || !a.seg_term[ch.seg]) return;  // k_scatter_stable's chunk
+  if (*((volatile const uint32_t*)a.err) & kErrNan) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  ModelDev md = a.models[ch.seg];
+  tree_top_to_smem<TREE, kTThreads>(md, a.k);
+  constexpr int kMain = TREE ? (int)kModelTree : (int)kModelLinear;
+  if (md.kind == kModelEq3)
+    scatter_term_chunk<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw);
+  else
+    scatter_term_chunk<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
 }
 
 // ------------------------------------------------------------------------------------
@@ -1927,10 +2149,9 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     const uint64_t* __restrict__ scr) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ uint64_t s_mbar[kWBWarps][2];
-  constexpr int BPL = kWBBins / 32;  // bins per lane
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   uint64_t* IN = reinterpret_cast<uint64_t*>(smraw + wp * kWBSmemPerWarp);  // 2 x kWBStride
-  uint32_t* bins = reinterpret_cast<uint32_t*>(IN + 2 * kWBStride);          // kWBBins + 32
+  uint32_t* bins = reinterpret_cast<uint32_t*>(IN + 2 * kWBStride);          // kWBBinWords
   uint64_t* mbar = s_mbar[wp];
   const uint32_t gw = blockIdx.x * kWBWarps + wp, gstride = gridDim.x * kWBWarps;
   // lane 0: start the bulk copy of the window described by wv into IN[b].  Descriptors are
@@ -2057,11 +2278,16 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     } else {
       const uint32_t nb = kWBBinsPerKey * len;
       const double scale = (double)nb / range;
-      // Bin f lives at bins[f + f / 32] (one pad word per 32 bins) so that the
-      // lane-contiguous scan walk is conflict-free.
-      for (uint32_t q = lane; q < (uint32_t)(kWBBins + 32); q += 32) bins[q] = 0u;
+      // Bin f lives at bins[f + 4 (f / 32)]: lane l's 16 bins are one 16-byte-aligned run, and
+      // the 8 lanes of a quarter-warp start on distinct 16-byte bank groups (conflict-free
+      // LDS.128 / STS.128 in the scan).
+      {
+        uint4* b4 = reinterpret_cast<uint4*>(bins);
+        for (uint32_t q = lane; q < (uint32_t)kWBBinWords / 4; q += 32) b4[q] = make_uint4(0, 0, 0, 0);
+      }
       __syncwarp();
-      uint32_t fr[kWBItems];  // bin
+      // histogram; the atomic's return is the key's arrival rank in its bin
+      uint32_t fr[kWBItems];  // bin | rank << 16
 #pragma unroll
       for (int j = 0; j < kWBItems; ++j) {
         fr[j] = 0;
@@ -2070,22 +2296,27 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
           if constexpr (F64) y = __longlong_as_double((long long)v[j]) - mn;
           else y = (double)(v[j] - umn);
           const uint32_t fb = min(__double2uint_rz(y * scale), nb - 1);
-          fr[j] = fb;
-          atomicAdd(&bins[fb + (fb >> 5)], 1u);
+          const uint32_t r = atomicAdd(&bins[wb_phys(fb)], 1u);
+          fr[j] = fb | (r << 16);
         }
       }
       __syncwarp();
-    WB_TICK(3);
-      // Lane l owns bins [BPL l, BPL l + BPL): after the scan its keys occupy B[lo, hi).
-      uint32_t mxc = 0, lo, hi;
+      // exclusive scan: lane l owns bins [16 l, 16 l + 16); counts -> starts in place
+      uint32_t mxc = 0, multi = 0;  // largest count; bins of this lane with 2..kFineOverflow keys
       {
-        uint32_t* bl0 = bins + lane * BPL + ((lane * BPL) >> 5);
+        uint4* lb = reinterpret_cast<uint4*>(bins + wb_phys(lane * kWBBpl));
+        uint4 c[kWBBpl / 4];
         uint32_t sum = 0;
-#pragma unroll 8
-        for (int q = 0; q < BPL; ++q) {
-          const uint32_t c = bl0[q];
-          sum += c;
-          mxc = max(mxc, c);
+#pragma unroll
+        for (int q = 0; q < kWBBpl / 4; ++q) {
+          c[q] = lb[q];
+          const uint32_t cs[4] = {c[q].x, c[q].y, c[q].z, c[q].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            sum += cs[e];
+            mxc = max(mxc, cs[e]);
+            multi |= (cs[e] >= 2u && cs[e] <= kFineOverflow ? 1u : 0u) << (4 * q + e);
+          }
         }
         uint32_t inc = sum;
 #pragma unroll
@@ -2093,46 +2324,34 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
           const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
           if (lane >= o) inc += y;
         }
-        lo = inc - sum;
-        hi = inc;
-        uint32_t run = lo;
-#pragma unroll 8
-        for (int q = 0; q < BPL; ++q) {
-          const uint32_t c = bl0[q];
-          bl0[q] = run;
-          run += c;
+        uint32_t run = inc - sum;
+#pragma unroll
+        for (int q = 0; q < kWBBpl / 4; ++q) {
+          uint4 o;
+          o.x = run; run += c[q].x;
+          o.y = run; run += c[q].y;
+          o.z = run; run += c[q].z;
+          o.w = run; run += c[q].w;
+          lb[q] = o;
         }
       }
       const bool overflow = __any_sync(0xffffffffu, mxc > kFineOverflow);
       __syncwarp();
-    WB_TICK(4);
+      // placement: bin start + arrival rank, in u64 key order (bits ^ flip)
 #pragma unroll
-      for (int j = 0; j < kWBItems; ++j) {
-        if (j * 32 + lane < len) {
-          const uint32_t fb = fr[j];
-          B[atomicAdd(&bins[fb + (fb >> 5)], 1u)] = v[j] ^ flip;  // u64 key order
-        }
-      }
+      for (int j = 0; j < kWBItems; ++j)
+        if (j * 32 + lane < len) B[bins[wb_phys(fr[j] & 0xffffu)] + (fr[j] >> 16)] = v[j] ^ flip;
       __syncwarp();
-    WB_TICK(5);
-      // bin f occupies B[bin_beg(f), bins[f + f / 32]) now (bins hold bin ends)
-      auto bin_beg = [&](uint32_t f) -> uint32_t { return f ? bins[(f - 1) + ((f - 1) >> 5)] : 0u; };
-      bool mixed = false;  // an overflowing bin holds different keys (not just duplicates)
-      uint32_t big = 0;    // this lane's bins above kFineOverflow keys
+      // A bin above kFineOverflow keys that holds one value (duplicates) needs no sorting;
+      // bins of different keys above it send the window to the bitonic sort.
+      bool mixed = false;
       if (overflow) {
-        if (mxc > kFineOverflow) {
-          uint32_t e0 = lo;
-          for (int q = 0; q < BPL; ++q) {
-            const uint32_t f = lane * BPL + q, e1 = bins[f + (f >> 5)];
-            big |= (e1 - e0 > kFineOverflow ? 1u : 0u) << q;
-            e0 = e1;
-          }
-        }
 #pragma unroll
         for (int j = 0; j < kWBItems; ++j) {
           if (j * 32 + lane < len) {
-            const uint32_t f = fr[j], b0 = bin_beg(f);
-            if (bins[f + (f >> 5)] - b0 > kFineOverflow && (v[j] ^ flip) != B[b0]) mixed = true;
+            const uint32_t f = fr[j] & 0xffffu;
+            const uint32_t b0 = bins[wb_phys(f)], b1 = f + 1 < nb ? bins[wb_phys(f + 1)] : len;
+            if (b1 - b0 > kFineOverflow && (v[j] ^ flip) != B[b0]) mixed = true;
           }
         }
         mixed = __any_sync(0xffffffffu, mixed);
@@ -2143,45 +2362,27 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
         warp_bitonic_ok<F64>(B, len, lane);
         OUT = B;
       } else {
-        // B is ordered across bins; each lane insertion-sorts its own range B[lo, hi): every
-        // key moves at most (its bin's load - 1) places.  The last two keys of the sorted
-        // prefix stay in registers (pp <= prev), so a key that moves by at most one place
-        // (nearly all of them) costs no branch; only a key below both walks the prefix.
-        // Bins above kFineOverflow keys hold one value each here (duplicates) and are skipped:
-        // the range is cut at their bounds and each piece is sorted alone.
-        uint32_t s0 = lo, msk = big;
-        while (true) {
-          uint32_t s1 = hi, nxt = 0;
-          if (msk) {  // next duplicate-only big bin: sort up to it, resume after it
-            const uint32_t f = lane * BPL + (__ffs(msk) - 1);
-            s1 = bin_beg(f);
-            nxt = bins[f + (f >> 5)];
-          }
-          if (s0 + 1 < s1) {
-            uint64_t* q = B + s0;  // q[1] is the key being inserted
-            uint64_t prev = q[0], pp = 0ull, nx = q[1];
-#pragma unroll 2
-            for (uint32_t i = s0 + 1; i < s1; ++i, ++q) {
-              const uint64_t x = nx;
-              nx = q[2];  // never written while x is inserted (may read past the piece)
-              const bool lt = x < prev;
-              const uint64_t m = max(pp, x);
-              if (lt) {
-                q[1] = prev;
-                q[0] = m;
-              }
-              if (lt && x < pp) {  // rare: x belongs below pp (q[0] = pp already)
-                uint64_t* r = q - 1;
-                while (r > B + s0 && r[-1] > x) { r[0] = r[-1]; --r; }
-                r[0] = x;
-              }
-              pp = lt ? m : prev;
-              prev = lt ? prev : x;
+        // B is ordered across bins; inside a bin the order is the atomics' arrival order.
+        // Every lane insertion-sorts its own bins of 2..kFineOverflow keys (~1.4 per lane at
+        // 2 bins per key), reading each bin's start back from the scan.
+        while (multi) {
+          const int jb = __ffs(multi) - 1;
+          multi &= multi - 1;
+          const uint32_t f = lane * kWBBpl + jb;
+          const uint32_t s = bins[wb_phys(f)];
+          const uint32_t e = f + 1 < nb ? bins[wb_phys(f + 1)] : len;
+          uint64_t* q = B + s;
+          if (e - s == 2) {  // ~70 % of the multi-key bins at 2 bins per key
+            const uint64_t x0 = q[0], x1 = q[1];
+            if (x0 > x1) { q[0] = x1; q[1] = x0; }
+          } else {
+            for (uint32_t i = 1; i < e - s; ++i) {
+              const uint64_t x = q[i];
+              uint32_t m = i;
+              while (m > 0 && q[m - 1] > x) { q[m] = q[m - 1]; --m; }
+              q[m] = x;
             }
           }
-          if (!msk) break;
-          msk &= msk - 1;
-          s0 = nxt;
         }
         oflip = flip;
         OUT = B;

@@ -543,3 +543,26 @@ def test_stale_status_words_cannot_pass_the_epoch_check(ipls, tag):
         t = dev(a)
         ipls.sort(t, k=1024, base_case=4096, key_type=0)
         assert host(t, np.float64).tobytes() == want.tobytes(), f"epoch {e0:#x}"
+
+
+@pytest.mark.parametrize("kind", ["normal", "dups", "presorted"])
+def test_match_rank_path_keeps_stable_layouts(ipls, kind):
+    """The stable scatter ranks keys by shared-memory atomics, whose same-address lanes B200
+    serves in lane order; every CTA probes that and otherwise ranks with match.any peer masks
+    (K3).  The probe has never failed on B200, so the fallback is forced here
+    (ipls_debug_force_match_rank): layouts after every level, models and the final array must
+    stay bit-exact with the oracle."""
+    rng = np.random.default_rng(len(kind))
+    n = 700_001
+    if kind == "normal":
+        a = rng.normal(0, 1, n)
+    elif kind == "dups":
+        a = rng.integers(0, 300, n).astype(np.float64)
+    else:
+        a = np.sort(rng.lognormal(0, 2, n))
+    ipls.lib().ipls_debug_force_match_rank(1)
+    try:
+        sort_parity_with_layouts(ipls, a, 256, 4096)
+        sort_parity_with_layouts(ipls, a, 1024, 1000)
+    finally:
+        ipls.lib().ipls_debug_force_match_rank(0)

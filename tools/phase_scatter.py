@@ -29,13 +29,11 @@ for rep in range(2):
     torch.cuda.synchronize()
 lib.ipls_debug_scatter_phases(ph, 1)
 tr = ipls.sort_trace(src.clone(), k=cfg.k, base_case=cfg.base_case, key_type=kt) if False else None
-tiles = sum((int(n) + 8191) // 8192 for n in [a.size]) * 2  # approx: 2 levels over all keys
-print("scatter cycles per tile (thread 0):", " ".join(f"{i}:{ph[i] / tiles:.0f}" for i in range(7)))
-nt = max(ph[15], 1)
-print(f"unstable scatter: {ph[15]} tiles; cycles per tile (thread 0): zero {ph[11]/nt:.0f} count {ph[12]/nt:.0f} "
-      f"scan {ph[13]/nt:.0f} place {ph[14]/nt:.0f} writeout {ph[7]/nt:.0f}")
+ns, nt = max(ph[28], 1), max(ph[29], 1)
+print(f"stable scatter: {ph[28]} tiles; cycles per tile (thread 0): ranks {ph[0]/ns:.0f} offsets {ph[1]/ns:.0f} "
+      f"place {ph[2]/ns:.0f} writeout {ph[3]/ns:.0f}")
+print(f"terminal scatter: {ph[29]} tiles; cycles per tile (thread 0): slots {ph[4]/nt:.0f} offsets {ph[5]/nt:.0f} "
+      f"place {ph[6]/nt:.0f} writeout {ph[7]/nt:.0f}")
 print(f"large-sample fit (1 CTA, cycles): gather {ph[16]} sort {ph[17]} fmcd {ph[18]}")
-print("small-sample fit sort sub-phases (cycles summed):", [ph[i] for i in range(22, 27)])
-print(f"small-sample fit (cycles summed over CTAs): gather {ph[19]} sort {ph[20]} fmcd {ph[21]}")
 print("fit cycle sums over all CTAs of the last sort (x1e6): gather", ph[8] / 1e6, "sort", ph[9] / 1e6,
       "fmcd", ph[10] / 1e6)

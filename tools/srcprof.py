@@ -3,12 +3,12 @@
 usage: python tools/srcprof.py REPORT.ncu-rep KERNEL_REGEX [TOP]
 Prints the source lines with the most warp-stall samples and executed warp instructions
 (ncu --page source --print-source cuda,sass; needs -lineinfo)."""
-import csv, io, subprocess, sys
+import csv, io, os, subprocess, sys
 
 rep, kre = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
-                      "-k", "regex:" + kre, "--launch-count", "1"], capture_output=True, text=True).stdout
+                      "-k", "regex:" + kre, "--launch-count", "1", "--launch-skip", os.environ.get("SKIP","0")], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 agg = []
 fname = ""
