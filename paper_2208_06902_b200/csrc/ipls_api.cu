@@ -447,18 +447,20 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
       IPLS_PROF("gather_fit", 0);
       const uint32_t cap = fit_cap(max_S);
       uint32_t* redo = at<uint32_t>(meta, ML.seg_term);  // scratch until K2 writes seg_term
+      uint32_t* redo_cnt = &cctr->n_redo;                 // zero: cleared with the counters
       if (max_S <= (uint32_t)kFMMax)
         k_fit_small<F64, kFSThreads, kFMItems><<<nseg, kFSThreads, kFMSmem, st>>>(
-            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree);
+            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
       else if (max_S <= (uint32_t)kFSMax)
         k_fit_small<F64, kFSThreads, kFSItems><<<nseg, kFSThreads, kFSSmem, st>>>(
-            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree);
+            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
       else
         k_fit_small<F64, kFLThreads, kFLItems><<<nseg, kFLThreads, kFLSmem, st>>>(
-            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree);
+            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
       ck_launch();
-      k_gather_fit<F64><<<nseg, kFitThreads, fit_smem(cap), st>>>(
-          src, segs, seed, level, k, cap, trace ? samples : nullptr, models, nullptr, redo, tree);
+      k_gather_fit<F64><<<std::min(nseg, num_sms()), kFitThreads, fit_smem(cap), st>>>(
+          src, segs, seed, level, k, cap, trace ? samples : nullptr, models, nullptr, redo, tree, 0,
+          redo_cnt);
       ck_launch();
     }
     LevelArgs la{};

@@ -250,15 +250,21 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
     uint32_t level, uint32_t k, uint32_t cap, uint64_t* __restrict__ samples_out,
     ModelDev* __restrict__ models, const uint64_t* __restrict__ presorted_ok,
-    const uint32_t* __restrict__ redo, uint64_t* __restrict__ tree, int sort_given = 0) {
-  if (redo && !redo[blockIdx.x]) return;  // fitted by k_fit_small
+    const uint32_t* __restrict__ redo, uint64_t* __restrict__ tree, int sort_given = 0,
+    const uint32_t* __restrict__ redo_cnt = nullptr) {
+  // With redo_cnt: the CTAs walk the list redo[0, *redo_cnt) of segments k_fit_small left over
+  // (usually none: a launch of a few idle CTAs).  Without: CTA s fits segment s.
+  const uint32_t nitems = redo_cnt ? *((volatile const uint32_t*)redo_cnt) : 1u;
+  for (uint32_t item = redo_cnt ? blockIdx.x : 0u; item < nitems; item += gridDim.x) {
+  const uint32_t sgi = redo_cnt ? redo[item] : blockIdx.x;
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* a = reinterpret_cast<uint64_t*>(smraw);   // cap
   uint64_t* tmp = a + cap;                             // cap
   uint32_t* fh = reinterpret_cast<uint32_t*>(tmp + cap);  // cap
   __shared__ SortSmem ss;
   __shared__ uint64_t s_pivot;
-  const SegDesc sg = segs[blockIdx.x];
+  __syncthreads();  // smem of the previous item
+  const SegDesc sg = segs[sgi];
   const uint32_t S = sg.S;
 #ifdef IPLS_SCATTER_TIMING
   long long ft_prev_ = clock64();
@@ -300,7 +306,7 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
   md.k_eff = k;
   bool eq3 = (sg.flags & kSegForceEq3) || S < 4;
   if (!eq3 && tree) {  // splitter-tree model instead of FMCD
-    uint64_t* hp = tree + (size_t)blockIdx.x * kMaxK;
+    uint64_t* hp = tree + (size_t)sgi * kMaxK;
     write_tree<kFitThreads>(a, S, k, hp);
     md.kind = kModelTree; md.heap = hp;
   } else if (!eq3) {
@@ -351,13 +357,14 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     md.pivot_ok = s_pivot; md.k_eff = 3;
   }
   FIT_TICK(10);
-  if (threadIdx.x == 0) models[blockIdx.x] = md;
+  if (threadIdx.x == 0) models[sgi] = md;
+  }
 }
 
 
 // Phases 1-3 for segments with S <= kFSMax samples: 256 threads, samples held in registers,
 // 3 CTAs per SM (the 1024-thread k_gather_fit below takes S > kFSMax, i.e. level 0 at 1e8
-// keys, and any segment whose sample overflows a fine bin; the flag redo[s] tells which).
+// keys, and any segment whose sample overflows a fine bin; they are listed in redo[]).
 // Same result as k_gather_fit: same sample, exact sort, Listing 1 by galloping + bisection.
 constexpr int kFSThreads = 256;
 constexpr int kFSItems = 20;                     // samples per thread
@@ -379,7 +386,7 @@ template <bool F64, int NT, int IT>
 __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
     const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
     uint32_t level, uint32_t k, uint64_t* __restrict__ samples_out, ModelDev* __restrict__ models,
-    uint32_t* __restrict__ redo, uint64_t* __restrict__ tree) {
+    uint32_t* __restrict__ redo, uint64_t* __restrict__ tree, uint32_t* __restrict__ redo_cnt) {
   constexpr int NW = NT / 32, SMAX = NT * IT;
   static_assert(NT >= 256 && IT % 4 == 0, "256 coarse bins, uint4 fine-bin scan");
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -391,7 +398,7 @@ __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
   const SegDesc sg = segs[blockIdx.x];
   const uint32_t S = sg.S;
   if (S > (uint32_t)SMAX) {
-    if (threadIdx.x == 0) redo[blockIdx.x] = 1u;
+    if (threadIdx.x == 0) redo[atomicAdd(redo_cnt, 1u)] = blockIdx.x;
     return;
   }
   // ---- stratified sample (R2, R18), as ordering keys in registers ----
@@ -566,7 +573,7 @@ __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
           if (st != ~0u && B[st] != v[r]) mixed = true;
         }
       if (__syncthreads_or(mixed)) {
-        if (threadIdx.x == 0) redo[blockIdx.x] = 1u;  // the 1024-thread kernel sorts it
+        if (threadIdx.x == 0) redo[atomicAdd(redo_cnt, 1u)] = blockIdx.x;  // the 1024-thread kernel sorts it
         return;
       }
     }
@@ -605,7 +612,6 @@ __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
   }
   __syncthreads();
   FITL_TICK(17);
-  if (threadIdx.x == 0) redo[blockIdx.x] = 0u;
   if (samples_out)
     for (uint32_t j = threadIdx.x; j < S; j += NT) samples_out[sg.sample_off + j] = B[j];
   if (threadIdx.x == 0) s_pivot = B[S / 2];
@@ -723,18 +729,27 @@ __device__ __forceinline__ void warp_add_u64(unsigned long long* dst, unsigned l
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
 }
 
+// Chunks of a segment at levels >= 1: round(m / chunk_keys) chunks of equal length (at least
+// one), i.e. 2/3 to 3/2 of chunk_keys each -- no small remainder chunk that would pay a CTA's
+// whole per-chunk setup for a few keys (a 97k-key segment used to become 96k + 1k).
+__host__ __device__ __forceinline__ uint32_t chunks_of(uint32_t m, uint32_t ck) {
+  const uint32_t n = (uint32_t)(((uint64_t)m + ck / 2) / ck);
+  return n ? n : 1u;
+}
+
 __device__ void emit_segment(const LevelArgs& a, uint64_t begin, uint32_t m, uint32_t flags,
                              uint32_t seg_idx, uint32_t samp_off, uint32_t ch_off) {
   SegDesc sd{};
   sd.begin = begin; sd.m = m; sd.S = sample_size(m, a.k); sd.sample_off = samp_off;
-  uint32_t nch = (m + a.chunk_keys - 1) / a.chunk_keys;
+  const uint32_t nch = chunks_of(m, a.chunk_keys);
+  const uint32_t per = (m + nch - 1) / nch;
   sd.chunk_first = ch_off; sd.nchunks = nch; sd.flags = flags;
   a.nsegs[seg_idx] = sd;
   atomicMax(&a.nctr->max_S, sd.S);
   for (uint32_t j = 0; j < nch; ++j) {
     ChunkDesc cd;
-    cd.start = begin + (uint64_t)j * a.chunk_keys;
-    cd.len = min(a.chunk_keys, m - j * a.chunk_keys);
+    cd.start = begin + (uint64_t)j * per;
+    cd.len = min(per, m - j * per);
     cd.seg = seg_idx;
     a.nchunks[ch_off + j] = cd;
   }
@@ -970,7 +985,7 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
     if (cm[q]) {
       w_seg += 1;
       w_samp += sample_size(cm[q], k);
-      w_ch += (cm[q] + a.chunk_keys - 1) / a.chunk_keys;
+      w_ch += chunks_of(cm[q], a.chunk_keys);
     }
   }
   uint32_t t_seg, t_samp, t_ch;
@@ -999,7 +1014,7 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
           nkeys += cm[q];
           i_seg += 1;
           i_samp += sample_size(cm[q], k);
-          i_ch += (cm[q] + a.chunk_keys - 1) / a.chunk_keys;
+          i_ch += chunks_of(cm[q], a.chunk_keys);
         }
       }
       warp_add_u64((unsigned long long*)&a.nctr->keys, nkeys);
