@@ -249,13 +249,30 @@ def main():
     st = torch.cuda.current_stream()
 
     model = ipls.MODEL_TREE if args.model == "tree" else ipls.MODEL_LINEAR
+    # L2 flush between the restore and the timed sort: a 256 MB write (> 126 MB L2) so that
+    # no part of the restored input is L2-resident when the step starts
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
     def one(timed_events=None):
         work.copy_(pristine)
+        flush.fill_(1)
         if timed_events is not None:
             timed_events[0].record(st)
         ipls.sort(work, k=cfg.k, base_case=cfg.base_case, key_type=kt, model=model)
         if timed_events is not None:
             timed_events[1].record(st)
+
+    # first call of a fresh stream: includes the library's workspace allocation (cudaMalloc)
+    first_stream = torch.cuda.Stream(device=dev)
+    work.copy_(pristine)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(first_stream):
+        e0f, e1f = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0f.record(first_stream)
+        ipls.sort(work, k=cfg.k, base_case=cfg.base_case, key_type=kt, model=model)
+        e1f.record(first_stream)
+    torch.cuda.synchronize()
+    first_call_ms = e0f.elapsed_time(e1f)
 
     for _ in range(args.warmup):
         one()
@@ -283,9 +300,23 @@ def main():
     clocks = sampler.stop()
     launches = ipls.launch_count() - launches0
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
-    ms_local = sum(step_ms) / len(step_ms)
+    ms_local = statistics.median(step_ms)  # BASELINE.md §2 / SPEC: median over repetitions
     ms = allreduce_max(ms_local, world)
+    ms_mean = allreduce_max(sum(step_ms) / len(step_ms), world)
     value = n * world / (ms / 1e3)
+
+    # context (not the target): torch.sort (CUB radix sort) of the same input on the device
+    tsort = []
+    for i in range(3):
+        src_t = pristine.view(torch.float64) if kt == ipls.KEY_F64 else pristine
+        flush.fill_(2)
+        e0t, e1t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0t.record(st)
+        torch.sort(src_t)
+        e1t.record(st)
+        torch.cuda.synchronize()
+        tsort.append(e0t.elapsed_time(e1t))
+    torch_sort_ms = statistics.median(tsort)
 
     # pass 2 (roofline): the same K steps again with a CUDA-event pair around every kernel
     # launch inside the library, on the stream the kernels run on
@@ -302,18 +333,27 @@ def main():
 
     # roofline of the dominant kernel (largest share of the step)
     peak, peak_kind = load_peaks()
-    tot_prof_ms = sum(v[1] for v in prof.values())
-    dom = max((k_ for k_ in prof if prof[k_][2] > 0), key=lambda k_: prof[k_][1])
+    # "scatter" brackets both scatter kernels of a level; scatter_stable / scatter_term are the
+    # two kernels inside it (shares are over the top-level entries only)
+    nested = {"scatter_stable", "scatter_term"}
+    tot_prof_ms = sum(v[1] for k_, v in prof.items() if k_ not in nested)
+    dom = max((k_ for k_ in prof if prof[k_][2] > 0 and k_ not in nested), key=lambda k_: prof[k_][1])
     d_launch, d_ms, d_bytes = prof[dom]
     achieved = d_bytes / (d_ms / 1e3) / 1e9
     traffic = args.traffic
+    traffic_src = "--traffic argument"
     if traffic is None:
-        try:
-            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-                traffic = json.load(f)["kernels"][dom]["dram_bytes_per_launch"]
-        except Exception:
-            traffic = None
-    shares = {k_: round(v[1] / tot_prof_ms, 4) for k_, v in sorted(prof.items())}
+        traffic_src = None
+        for tf in ("r02_traffic.json", "r01_traffic.json"):
+            try:
+                with open(os.path.join(ROOT, "profiles", tf)) as f:
+                    traffic = json.load(f)["kernels"][dom]["dram_bytes_per_launch"]
+                traffic_src = (f"not measured in this run: ncu dram__bytes_read.sum + "
+                               f"dram__bytes_write.sum per launch from profiles/{tf}")
+                break
+            except Exception:
+                traffic = None
+    shares = {k_: round(v[1] / tot_prof_ms, 4) for k_, v in sorted(prof.items()) if k_ not in nested}
     per_kernel = {k_: {"launches": v[0], "ms_per_step": round(v[1] / args.steps, 4),
                        "alg_GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1) if v[2] > 0 else None}
                   for k_, v in sorted(prof.items())}
@@ -358,8 +398,18 @@ def main():
                 "workload": f"{args.config}: {cfg.desc}, n={n}, k={cfg.k}, base_case={cfg.base_case}",
                 "model": args.model,
                 "parallelism": "replicas" if world > 1 else "single-gpu",
-                "l2": "input 0.8 GB > L2 126 MB; pristine copy restored (D2D) before every step",
-                "timing": "CUDA events around each ipls_sort_ex call on its stream; mean over steps; max over ranks",
+                "l2": "input 0.8 GB > L2 126 MB; pristine copy restored (D2D) and a 256 MB "
+                      "buffer written (L2 flush) before every step, both outside the timed region",
+                "timing": "CUDA events around each ipls_sort_ex call on its stream; median over "
+                          "steps (mean %.4f ms); max over ranks" % ms_mean,
+                "first_call_ms": round(first_call_ms, 3),
+                "first_call_note": "first sort on a fresh stream: includes the workspace "
+                                   "allocation; every timed step reuses the stream's workspace",
+                "context_torch_sort": {"ms": round(torch_sort_ms, 3),
+                                       "keys_per_s": n / (torch_sort_ms / 1e3),
+                                       "note": "torch.sort of the same device tensor (CUB "
+                                               "radix sort, values and indices), median of 3; "
+                                               "context, not the target"},
                 "per_kernel_timing": "second pass of the same K steps with a CUDA-event pair around "
                                      "every kernel inside the library (its ms_per_step: "
                                      f"{ms_prof:.4f}); shares and roofline come from that pass",
@@ -374,6 +424,7 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "alg_bytes_per_launch": d_bytes / max(d_launch, 1)},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,

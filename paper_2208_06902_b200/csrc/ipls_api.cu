@@ -204,8 +204,10 @@ MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_
   return L;
 }
 
+// The caller-workspace path never traces, and the level's sorted samples are kept only for
+// the trace (the fit kernels keep them on chip), so the worst case reserves no sample space.
 size_t worst_meta_bytes(const Params& p) {
-  return meta_layout(p.cap_segs, p.cap_chunks, p.cap_samples, p.k, p.tree).total;
+  return meta_layout(p.cap_segs, p.cap_chunks, 0, p.k, p.tree).total;
 }
 
 // Device buffers for one call: either the caller's workspace or the per-stream cache.
@@ -414,7 +416,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     Fill* fills = at<Fill>(fixed, FL.fills[cur]);
 
     // per-level metadata, sized by this level's actual counts
-    const MetaLayout ML = meta_layout(nseg, nchunk, nsample, k, p.tree);
+    const MetaLayout ML = meta_layout(nseg, nchunk, trace ? nsample : 0, k, p.tree);
     void* meta = d_meta_in;
     if (meta_cache) {
       meta_cache->ensure(ML.total);
