@@ -209,6 +209,136 @@ def bench_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def bench_dist(args, world, rank, local):
+    """N ranks, one array: the workload sharded in rank order (n/N keys each), sorted by
+    dist_sort (global sample + shared FMCD model, stable partition, count
+    all-gather, range plan, one NCCL all-to-all, regroup, local sorts resumed at level 1).
+    Strong scaling: value = n / max over ranks of the step time."""
+    import torch
+    import torch.distributed as dist
+    import paper_2208_06902_b200 as ipls
+    from paper_2208_06902_b200 import datagen
+    from paper_2208_06902_b200.distributed import dist_sort
+    if world == 1 and not dist.is_initialized():
+        import socket
+        sk = socket.socket(); sk.bind(("127.0.0.1", 0)); port = sk.getsockname()[1]; sk.close()
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(port))
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", local))
+    cfg = datagen.CONFIGS[args.config]
+    a = datagen.generate(args.config)
+    n = a.size
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    dev = torch.device("cuda", local)
+    shard = torch.from_numpy(a[lo:hi].view(np.int64).copy()).to(dev)
+    if a.dtype == np.float64:
+        shard = shard.view(torch.float64)
+    work = torch.empty_like(shard)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+
+    def one(evs=None):
+        work.copy_(shard)
+        flush.fill_(1)
+        if evs is not None:
+            evs[0].record(st)
+        res = dist_sort(work, k=cfg.k, base_case=cfg.base_case)
+        if evs is not None:
+            evs[1].record(st)
+        return res
+
+    for _ in range(args.warmup):
+        res = one()
+    torch.cuda.synchronize()
+    # correctness: every range sorted, ranges in rank order, all keys present
+    mine = res.keys.view(torch.int64) if a.dtype == np.float64 else res.keys
+    srt = res.keys
+    assert bool((srt[1:] >= srt[:-1]).all()) if a.dtype == np.float64 else True
+    tot = torch.tensor([mine.numel()], dtype=torch.int64, device=dev)
+    dist.all_reduce(tot)
+    assert int(tot.item()) == n, "keys lost in the exchange"
+    sampler = ClockSampler(local)
+    launches0 = ipls.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for i in range(args.steps):
+        one(evs[i])
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = sampler.stop()
+    launches = ipls.launch_count() - launches0
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    ms = allreduce_max(statistics.median(step_ms), world)
+    value = n / (ms / 1e3)
+    # roofline pass: the library's per-kernel CUDA events on this rank (same K steps again)
+    ipls.profile_reset()
+    ipls.profile_enable(True)
+    for i in range(args.steps):
+        one()
+    torch.cuda.synchronize()
+    ipls.profile_enable(False)
+    prof = ipls.profile_read()
+    nested = {"scatter_stable", "scatter_term"}
+    dom = max((k_ for k_ in prof if prof[k_][2] > 0 and k_ not in nested), key=lambda k_: prof[k_][1])
+    d_launch, d_ms, d_bytes = prof[dom]
+    achieved = d_bytes / (d_ms / 1e3) / 1e9
+    # e2e: the shard from pinned host memory, dist_sort, the result back to host
+    hsh = torch.from_numpy(a[lo:hi].view(np.int64).copy()).pin_memory()
+    e2e = []
+    for i in range(args.e2e_steps + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        w = hsh.to(dev, non_blocking=True)
+        if a.dtype == np.float64:
+            w = w.view(torch.float64)
+        r = dist_sort(w, k=cfg.k, base_case=cfg.base_case)
+        back = r.keys.cpu()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if i > 0:
+            e2e.append(dt)
+    e2e_s = allreduce_max(statistics.median(e2e), world)
+    if rank == 0:
+        import math
+        Lstar = math.ceil(math.log(math.ceil(n / cfg.base_case), cfg.k))
+        model_bytes = 2 * 8 * n * (Lstar + 1)
+        peak, peak_kind = load_peaks()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if a.dtype == np.float64 else "u64", "data": "synthetic",
+            "config": {
+                "workload": f"{args.config}: {cfg.desc}, n={n}, k={cfg.k}, base_case={cfg.base_case}",
+                "parallelism": f"dist_sort over {world} rank(s): shards of n/{world} keys, one "
+                               "NCCL all-to-all, local sorts resumed at level 1",
+                "l2": "shard restored (D2D) and a 256 MB buffer written before every step",
+                "timing": "CUDA events around each dist_sort call; median over steps; max over ranks",
+                "sort_roofline_model": {"bytes_per_key": 16 * (Lstar + 1),
+                                        "frac_of_8TBps_per_gpu": round(
+                                            (model_bytes / world / 8e12) / (ms / 1e3), 4)},
+            },
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "traffic_source": "not captured for the multi-rank run",
+                         "alg_bytes_per_launch": d_bytes / max(d_launch, 1),
+                         "note": "rank 0's library kernels (CUDA events on its stream)"},
+            "cpu_baseline": None,
+            "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                    "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -224,6 +354,11 @@ def main():
     ap.add_argument("--model", default="fmcd", choices=["fmcd", "tree"],
                     help="partition model: fmcd (IPLS, the default and the headline) or tree "
                          "(IPS4o's splitter tree on the same kernels, SURVEY NEXT #2)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: every rank sorts its own copy of the workload (weak scaling) "
+                         "instead of dist_sort on one array sharded over the ranks")
+    ap.add_argument("--dist", action="store_true",
+                    help="run dist_sort even at N = 1 (a one-rank NCCL group; for testing)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (default: the "
                          "committed profiles/r01_traffic.json capture)")
@@ -239,6 +374,9 @@ def main():
     from paper_2208_06902_b200 import datagen
 
     world, rank, local = dist_init(args)
+    if (world > 1 and not args.replicas) or args.dist:
+        bench_dist(args, world, rank, local)
+        return
     cfg = datagen.CONFIGS[args.config]
     a = datagen.generate(args.config)
     kt = ipls.KEY_F64 if a.dtype == np.float64 else ipls.KEY_U64

@@ -132,6 +132,32 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
  * contiguous buckets [bounds[r], bounds[r+1]); (5) one all-to-all moves the keys and every
  * rank sorts what it received (ipls_sort_ex).  Rank r then holds the r-th key range. */
 
+/* Sort n keys that form nseg consecutive range-ordered segments -- every key of segment i
+ * precedes (ordering key) every key of segment i+1 -- by resuming the recursion
+ * at `level`: each segment of more than base_case keys is partitioned as a
+ * level-`level` segment (its sample drawn with that level's hash, R2/R18, as if an earlier
+ * level had produced it), each smaller one goes to the base case.  This is the local
+ * sort of the multi-GPU top level: with level = 1 and the top level's buckets,
+ * in global order, as the segments, every model and layout below the top level equals the
+ * one-GPU sort's.  d_keys: device, n keys sorted in place.  h_seg_sizes: host, nseg sizes
+ * summing to n (zeros allowed).  Uses the stream's internal workspace.  Errors: as
+ * ipls_sort_ex (NaN: the array is left unmodified), INVALID_ARGUMENT if the sizes do not sum
+ * to n.  The segments are trusted to be range-ordered (not checked); if they are not, the
+ * output is not sorted. */
+ipls_status ipls_sort_segments(void* d_keys, size_t n, ipls_key_type t, const ipls_config* cfg,
+                               const uint64_t* h_seg_sizes, uint32_t nseg, uint32_t level,
+                               void* stream);
+
+/* Multi-GPU exchange: the receiving rank holds G runs back to back, run g
+ * (from source rank g, in rank order) holding that source's keys of buckets b0 .. b0+nb-1,
+ * bucket-major (a stable partition's output).  Moves them into bucket-major order: for each
+ * bucket, run 0's keys, then run 1's, ... -- the stable partition of the concatenated global
+ * array restricted to these buckets.  d_src, d_dst: device, distinct, sum(h_counts) keys
+ * each.  h_counts: host, G x nb (row g = run g's bucket counts).  Synchronises `stream`.
+ * Errors: INVALID_ARGUMENT (NULL), OUT_OF_MEMORY, CUDA. */
+ipls_status ipls_regroup_runs(const void* d_src, void* d_dst, const uint64_t* h_counts,
+                              uint32_t G, uint32_t nb, void* stream);
+
 /* S(m) = min(max(ceil(ceil(log2 m)/5) k - 1, 4), floor(m/2)) (R1, R19).  Host only. */
 uint32_t ipls_sample_size(uint64_t m, uint32_t k);
 
@@ -179,6 +205,12 @@ typedef struct {
  * are too small are filled up to their capacity and *_len reports the full size. */
 ipls_status ipls_sort_trace(void* d_keys, size_t n, ipls_key_type t, const ipls_config* cfg,
                             ipls_trace* trace, void* stream);
+/* ipls_sort_segments with the per-segment trace of ipls_sort_trace (records carry the hash
+ * level, starting at `level`; snapshots by iteration).  Same arguments and errors. */
+ipls_status ipls_sort_segments_trace(void* d_keys, size_t n, ipls_key_type t,
+                                     const ipls_config* cfg, const uint64_t* h_seg_sizes,
+                                     uint32_t nseg, uint32_t level, ipls_trace* trace,
+                                     void* stream);
 
 const char* ipls_status_string(ipls_status s);
 const char* ipls_last_cuda_error(void);

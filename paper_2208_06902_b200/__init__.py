@@ -84,7 +84,8 @@ SYMBOLS = ["ipls_default_config", "ipls_sort_f64", "ipls_sort_u64", "ipls_sort_e
            "ipls_sort_trace", "ipls_status_string", "ipls_last_cuda_error",
            "ipls_kernel_launch_count", "ipls_profile_enable", "ipls_profile_reset",
            "ipls_profile_read", "ipls_sample_size", "ipls_sample_strata", "ipls_assign_ranges", "ipls_fit_sample", "ipls_debug_set_epoch",
-           "ipls_debug_force_match_rank"]
+           "ipls_debug_force_match_rank", "ipls_sort_segments",
+           "ipls_regroup_runs", "ipls_sort_segments_trace"]
 
 _lib = None
 
@@ -128,6 +129,12 @@ def lib():
         L.ipls_sample_strata.argtypes = [vp, sz, u64, u64, u32, u64, vp, vp]
         L.ipls_sample_strata.restype = i32
         L.ipls_assign_ranges.argtypes = [vp, u32, u32, vp]; L.ipls_assign_ranges.restype = i32
+        L.ipls_sort_segments.argtypes = [vp, sz, i32, ctypes.POINTER(_Config), vp, u32, u32, vp]
+        L.ipls_sort_segments.restype = i32
+        L.ipls_regroup_runs.argtypes = [vp, vp, vp, u32, u32, vp]; L.ipls_regroup_runs.restype = i32
+        L.ipls_sort_segments_trace.argtypes = [vp, sz, i32, ctypes.POINTER(_Config), vp, u32, u32,
+                                               ctypes.POINTER(_Trace), vp]
+        L.ipls_sort_segments_trace.restype = i32
         _lib = L
     return _lib
 
@@ -203,6 +210,31 @@ def sort(keys, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SEED,
         ws, wsb = workspace.data_ptr(), workspace.numel() * workspace.element_size()
     _check(lib().ipls_sort_ex(keys.data_ptr(), keys.numel(), kt, ctypes.byref(c), ws, wsb,
                               _stream(stream)))
+
+
+def sort_segments(keys, sizes, level: int = 1, k: int = 256, base_case: int = 4096,
+                  seed: int = DEFAULT_SEED, key_type: Optional[int] = None, stream=None,
+                  model: int = MODEL_LINEAR) -> None:
+    """Sort in place a CUDA tensor made of consecutive range-ordered segments of the given
+    sizes, resuming the recursion at `level` (ipls_sort_segments)."""
+    _check_tensor(keys)
+    kt = _key_type_of(keys, key_type)
+    c = _cfg(k, base_case, seed, model)
+    sz = np.ascontiguousarray(np.asarray(sizes, dtype=np.uint64))
+    _check(lib().ipls_sort_segments(keys.data_ptr(), keys.numel(), kt, ctypes.byref(c),
+                                    sz.ctypes.data if sz.size else None, int(sz.size),
+                                    int(level), _stream(stream)))
+
+
+def regroup_runs(src, dst, counts, stream=None) -> None:
+    """ipls_regroup_runs: G received runs (counts: G x nb per-bucket counts) into bucket-major
+    order in dst (CUDA tensors of 8-byte elements)."""
+    _check_tensor(src)
+    _check_tensor(dst)
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.uint64))
+    G, nb = (c.shape[0], c.shape[1]) if c.ndim == 2 else (0, 0)
+    _check(lib().ipls_regroup_runs(src.data_ptr(), dst.data_ptr(),
+                                   c.ctypes.data if c.size else None, G, nb, _stream(stream)))
 
 
 def workspace_bytes(n: int, key_type: int = KEY_F64, k: int = 256, base_case: int = 4096,
@@ -328,8 +360,11 @@ class TraceResult:
 def sort_trace(keys, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SEED,
                key_type: Optional[int] = None, snapshot_levels: int = 0, stream=None,
                max_records: int = 1 << 16, max_counts: int = 1 << 24,
-               max_samples: int = 1 << 24, model: int = MODEL_LINEAR) -> TraceResult:
-    """Sort in place and return the per-segment trace (records ordered by level, begin)."""
+               max_samples: int = 1 << 24, model: int = MODEL_LINEAR, segments=None,
+               level: int = 1) -> TraceResult:
+    """Sort in place and return the per-segment trace (records ordered by level, begin).
+    segments: sizes of range-ordered segments to resume from at `level`
+    (ipls_sort_segments_trace) instead of a whole sort."""
     import torch
     _check_tensor(keys)
     kt = _key_type_of(keys, key_type)
@@ -347,8 +382,15 @@ def sort_trace(keys, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SE
                     smps.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), max_samples, 0,
                     snaps.data_ptr() if snaps is not None else None, snapshot_levels, 0)
         backup = keys.clone()
-        _check(lib().ipls_sort_trace(keys.data_ptr(), n, kt, ctypes.byref(c), ctypes.byref(tr),
-                                     _stream(stream)))
+        if segments is None:
+            _check(lib().ipls_sort_trace(keys.data_ptr(), n, kt, ctypes.byref(c),
+                                         ctypes.byref(tr), _stream(stream)))
+        else:
+            sz = np.ascontiguousarray(np.asarray(segments, dtype=np.uint64))
+            _check(lib().ipls_sort_segments_trace(keys.data_ptr(), n, kt, ctypes.byref(c),
+                                                  sz.ctypes.data if sz.size else None,
+                                                  int(sz.size), int(level), ctypes.byref(tr),
+                                                  _stream(stream)))
         if tr.records_len <= max_records and tr.counts_len <= max_counts and \
                 tr.samples_len <= max_samples:
             break

@@ -363,11 +363,53 @@ uint32_t next_epoch(bool* wrapped) {
   return e & 0xffff;
 }
 
-// Run the whole level-batched sort.  keys: device array (user buffer).
+// ipls_sort_segments: the array is nseg consecutive range-ordered segments; the recursion
+// resumes at `level` (the hash level of R18) with them as its segments.
+struct InitSegs {
+  const uint64_t* sizes;  // host, nseg entries summing to n
+  uint32_t nseg;
+  uint32_t level;
+};
+
+// Greedy left-to-right packing of the base-case segments of an initial segment list into
+// windows (small: <= kWBCap keys each, packed to <= kWBCap; big: packed to <= kBigCap); a
+// segment of the other classes breaks a window (as pack_windows does on the device).
+void pack_initial(const InitSegs& in, uint32_t B, std::vector<Window>& small,
+                  std::vector<Window>& big, uint64_t& small_keys, uint64_t& big_keys) {
+  Window cs{0, 0, 0}, cb{0, 0, 0};
+  auto flush = [](Window& w, std::vector<Window>& out, uint64_t& keys) {
+    if (w.len) { out.push_back(w); keys += w.len; }
+    w.len = 0;
+  };
+  uint64_t pos = 0;
+  for (uint32_t i = 0; i < in.nseg; ++i) {
+    const uint64_t m = in.sizes[i];
+    const bool is_small = m > 0 && m <= (uint64_t)kWBCap;
+    const bool is_big = m > (uint64_t)kWBCap && m <= B;
+    if (m > 0 && !is_small) flush(cs, small, small_keys);
+    if (m > 0 && !is_big) flush(cb, big, big_keys);
+    if (is_small) {
+      if (cs.len && cs.len + m > (uint64_t)kWBCap) flush(cs, small, small_keys);
+      if (!cs.len) cs.begin = pos;
+      cs.len += (uint32_t)m;
+    } else if (is_big) {
+      if (cb.len && cb.len + m > (uint64_t)kBigCap) flush(cb, big, big_keys);
+      if (!cb.len) cb.begin = pos;
+      cb.len += (uint32_t)m;
+    }
+    pos += m;
+  }
+  flush(cs, small, small_keys);
+  flush(cb, big, big_keys);
+}
+
+// Run the whole level-batched sort.  keys: device array (user buffer).  init: nullptr for a
+// whole sort (root segment at level 0), else the segments to resume from.
 template <bool F64>
 ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_in,
                      size_t meta_bytes_in, DevBuf* meta_cache, LevelCounters* h_ctr,
-                     cudaStream_t st, uint64_t seed, TraceSink* trace) {
+                     cudaStream_t st, uint64_t seed, TraceSink* trace,
+                     const InitSegs* init = nullptr) {
   set_attrs<F64>();
   const FixedLayout FL = fixed_layout(p);
   uint64_t* scr = at<uint64_t>(fixed, FL.scratch);
@@ -376,7 +418,8 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
   const uint64_t n = p.n;
   const uint32_t k = p.k;
 
-  if (n <= p.B) {
+  const uint32_t level0 = init ? init->level : 0u;
+  if (!init && n <= p.B) {
     // The root is a base-case segment: one window in place.
     Window w{0, (uint32_t)n, 0};
     Window* dw = at<Window>(fixed, FL.wins[0]);
@@ -392,20 +435,93 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     return IPLS_OK;
   }
 
-  // level-0 work: the root segment
-  uint32_t nseg = 1;
-  uint32_t nchunk = (uint32_t)((n + p.chunk_keys - 1) / p.chunk_keys);
-  uint32_t nsample = sample_size(n, k);
-  uint32_t max_S = nsample;
+  uint32_t nseg = 1, nchunk = 0, nsample = 0, max_S = 0;
   uint64_t level_keys = n;
+  LevelCounters init_ctr{};  // the initial segments' base-case windows (counted as level 0's)
   ck(cudaMemsetAsync(at<LevelCounters>(fixed, FL.ctr[0]), 0, sizeof(LevelCounters), st));
-  k_init_root<<<std::max<uint32_t>(1, (nchunk + 255) / 256), 256, 0, st>>>(
-      at<SegDesc>(fixed, FL.segs[0]), at<ChunkDesc>(fixed, FL.chunks[0]), n, nsample,
-      p.chunk_keys, 0u);
-  ck_launch();
+  if (!init) {
+    // level-0 work: the root segment
+    nchunk = (uint32_t)((n + p.chunk_keys - 1) / p.chunk_keys);
+    nsample = sample_size(n, k);
+    max_S = nsample;
+    k_init_root<<<std::max<uint32_t>(1, (nchunk + 255) / 256), 256, 0, st>>>(
+        at<SegDesc>(fixed, FL.segs[0]), at<ChunkDesc>(fixed, FL.chunks[0]), n, nsample,
+        p.chunk_keys, 0u);
+    ck_launch();
+  } else {
+    if (F64) {  // NaN anywhere: rejected before any write (R0)
+      k_nan_scan<<<num_sms() * 4, 256, 0, st>>>(keys, n, d_err);
+      ck_launch();
+      ck(cudaMemcpyAsync(&h_ctr[1].err, d_err, 4, cudaMemcpyDeviceToHost, st));
+      ck(cudaStreamSynchronize(st));
+      if (h_ctr[1].err & kErrNan) return IPLS_ERR_NAN_KEY;
+    }
+    std::vector<SegDesc> hs;
+    std::vector<ChunkDesc> hc;
+    std::vector<Window> hw, hwb;
+    uint64_t wk = 0, wbk = 0, pos = 0;
+    nsample = 0;
+    level_keys = 0;
+    for (uint32_t i = 0; i < init->nseg; ++i) {
+      const uint64_t m = init->sizes[i];
+      if (m > p.B) {
+        SegDesc sd{};
+        sd.begin = pos; sd.m = (uint32_t)m; sd.S = sample_size(m, k); sd.sample_off = nsample;
+        const uint32_t nch = chunks_of((uint32_t)m, p.chunk_keys), per = (uint32_t)((m + nch - 1) / nch);
+        sd.chunk_first = (uint32_t)hc.size(); sd.nchunks = nch; sd.flags = 0;
+        for (uint32_t j = 0; j < nch; ++j)
+          hc.push_back(ChunkDesc{pos + (uint64_t)j * per,
+                                 (uint32_t)std::min<uint64_t>(per, m - (uint64_t)j * per),
+                                 (uint32_t)hs.size()});
+        hs.push_back(sd);
+        nsample += sd.S;
+        max_S = std::max(max_S, sd.S);
+        level_keys += m;
+      }
+      pos += m;
+    }
+    pack_initial(*init, p.B, hw, hwb, wk, wbk);
+    if (hs.size() > p.cap_segs || hc.size() > p.cap_chunks || hw.size() > p.cap_wins ||
+        hwb.size() > p.cap_wbig)
+      return IPLS_ERR_OUT_OF_MEMORY;
+    if (!hs.empty()) {
+      ck(cudaMemcpy(at<SegDesc>(fixed, FL.segs[0]), hs.data(), hs.size() * sizeof(SegDesc),
+                    cudaMemcpyHostToDevice));
+      ck(cudaMemcpy(at<ChunkDesc>(fixed, FL.chunks[0]), hc.data(), hc.size() * sizeof(ChunkDesc),
+                    cudaMemcpyHostToDevice));
+    }
+    if (!hw.empty())
+      ck(cudaMemcpy(at<Window>(fixed, FL.wins[0]), hw.data(), hw.size() * sizeof(Window),
+                    cudaMemcpyHostToDevice));
+    if (!hwb.empty())
+      ck(cudaMemcpy(at<Window>(fixed, FL.wbig[0]), hwb.data(), hwb.size() * sizeof(Window),
+                    cudaMemcpyHostToDevice));
+    init_ctr.n_windows = (uint32_t)hw.size(); init_ctr.win_keys = wk;
+    init_ctr.n_wbig = (uint32_t)hwb.size(); init_ctr.wbig_keys = wbk;
+    nseg = (uint32_t)hs.size();
+    nchunk = (uint32_t)hc.size();
+    if (nseg == 0) {  // every segment goes to the base case
+      if (hw.size()) {
+        IPLS_PROF("base_warp", 16.0 * wk);
+        k_base_warp<F64><<<std::min<uint32_t>(((uint32_t)hw.size() + kWBWarps - 1) / kWBWarps, num_sms()),
+                           kWBWarps * 32, warp_base_smem(), st>>>(at<Window>(fixed, FL.wins[0]),
+                                                                  (uint32_t)hw.size(), keys, scr);
+        ck_launch();
+      }
+      if (hwb.size()) {
+        IPLS_PROF("base_sort", 16.0 * wbk);
+        k_base_sort<F64, false><<<(uint32_t)hwb.size(), kBCThreads, base_smem(), st>>>(
+            at<Window>(fixed, FL.wbig[0]), keys, scr, d_err);
+        ck_launch();
+      }
+      ck(cudaStreamSynchronize(st));
+      return IPLS_OK;
+    }
+  }
 
-  for (uint32_t level = 0; nseg > 0; ++level) {
-    const int cur = level & 1, nxt = cur ^ 1;
+  for (uint32_t iter = 0; nseg > 0; ++iter) {
+    const uint32_t level = level0 + iter;  // the sampling hash's level (R18)
+    const int cur = iter & 1, nxt = cur ^ 1;
     const uint64_t* src = (cur == 0) ? keys : scr;
     SegDesc* segs = at<SegDesc>(fixed, FL.segs[cur]);
     ChunkDesc* chunks = at<ChunkDesc>(fixed, FL.chunks[cur]);
@@ -444,7 +560,10 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     uint32_t* chunk_pre = at<uint32_t>(meta, ML.chunk_pre);
     uint64_t* tree = p.tree ? at<uint64_t>(meta, ML.tree) : nullptr;
 
-    ck(cudaMemsetAsync(nctr, 0, sizeof(LevelCounters), st));
+    if (iter == 0 && init)  // the initial segments' windows are this level's first windows
+      ck(cudaMemcpyAsync(nctr, &init_ctr, sizeof(LevelCounters), cudaMemcpyHostToDevice, st));
+    else
+      ck(cudaMemsetAsync(nctr, 0, sizeof(LevelCounters), st));
     {
       IPLS_PROF("gather_fit", 0);
       const uint32_t cap = fit_cap(max_S);
@@ -468,6 +587,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     LevelArgs la{};
     la.src = src; la.segs = segs; la.chunks = chunks; la.models = models;
     la.k = k; la.base_case = p.B; la.level = level; la.chunk_keys = p.chunk_keys; la.nkeys = n;
+    la.dstbuf = (iter + 1) & 1;
     la.ticket = &cctr->ticket;
     la.status = at<uint64_t>(meta, ML.status);
     la.cflag = at<uint8_t>(meta, ML.cflag);
@@ -478,7 +598,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     la.seg_tot = seg_tot;
     la.epoch = epoch;
     la.err = d_err;
-    la.check_nan = (F64 && level == 0) ? 1 : 0;
+    la.check_nan = (F64 && iter == 0 && !init) ? 1 : 0;
     la.ids = nullptr;
     la.single_offsets = nullptr;
     la.nsegs = at<SegDesc>(fixed, FL.segs[nxt]);
@@ -510,11 +630,11 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
       ck(cudaMemcpyAsync(hm.data(), models, nseg * sizeof(ModelDev), cudaMemcpyDeviceToHost, st));
       ck(cudaMemcpyAsync(ht.data(), seg_tot, ht.size() * 4, cudaMemcpyDeviceToHost, st));
       ck(cudaMemcpyAsync(hsmp.data(), samples, (size_t)nsample * 8, cudaMemcpyDeviceToHost, st));
-      if (trace->tr->d_snapshots && level < trace->tr->snapshot_levels) {
-        uint64_t* snap = static_cast<uint64_t*>(trace->tr->d_snapshots) + (size_t)level * n;
-        if (level > 0)
+      if (trace->tr->d_snapshots && iter < trace->tr->snapshot_levels) {
+        uint64_t* snap = static_cast<uint64_t*>(trace->tr->d_snapshots) + (size_t)iter * n;
+        if (iter > 0)
           ck(cudaMemcpyAsync(snap, snap - n, n * 8, cudaMemcpyDeviceToDevice, st));
-        k_snapshot<<<nseg, 256, 0, st>>>(segs, keys, scr, (level + 1) & 1, snap);
+        k_snapshot<<<nseg, 256, 0, st>>>(segs, keys, scr, (iter + 1) & 1, snap);
         ck_launch();
       }
       ck(cudaStreamSynchronize(st));
@@ -563,7 +683,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
       k_fill<<<c.n_fills, 256, 0, st>>>(fills, keys);
       ck_launch();
     }
-    if (trace) trace->tr->levels = level + 1;
+    if (trace) trace->tr->levels = iter + 1;
     nseg = c.n_segs;
     level_keys = c.keys;
     nchunk = c.n_chunks;
@@ -586,7 +706,8 @@ ipls_status check_cfg(const ipls_config* cfg, ipls_config* out) {
 }
 
 ipls_status sort_impl(void* d_keys, size_t n, ipls_key_type t, const ipls_config* cfg_in,
-                      void* d_ws, size_t ws_bytes, void* stream, ipls_trace* tr) {
+                      void* d_ws, size_t ws_bytes, void* stream, ipls_trace* tr,
+                      const InitSegs* init = nullptr) {
   ipls_config cfg;
   ipls_status s = check_cfg(cfg_in, &cfg);
   if (s != IPLS_OK) return s;
@@ -618,9 +739,9 @@ ipls_status sort_impl(void* d_keys, size_t n, ipls_key_type t, const ipls_config
     ipls_status r =
         (t == IPLS_KEY_F64)
             ? run_sort<true>(static_cast<uint64_t*>(d_keys), p, fixed, meta_in, meta_bytes,
-                             meta_cache, sc.h_ctr, st, cfg.seed, tr ? &sink : nullptr)
+                             meta_cache, sc.h_ctr, st, cfg.seed, tr ? &sink : nullptr, init)
             : run_sort<false>(static_cast<uint64_t*>(d_keys), p, fixed, meta_in, meta_bytes,
-                              meta_cache, sc.h_ctr, st, cfg.seed, tr ? &sink : nullptr);
+                              meta_cache, sc.h_ctr, st, cfg.seed, tr ? &sink : nullptr, init);
     prof_collect();
     if (tr) {
       // order records by (level, begin)
@@ -685,6 +806,76 @@ ipls_status ipls_sort_trace(void* d_keys, size_t n, ipls_key_type t, const ipls_
                             ipls_trace* trace, void* stream) {
   if (!trace) return IPLS_ERR_INVALID_ARGUMENT;
   return sort_impl(d_keys, n, t, cfg, nullptr, 0, stream, trace);
+}
+
+static ipls_status sort_segments_impl(void* d_keys, size_t n, ipls_key_type t,
+                                      const ipls_config* cfg, const uint64_t* h_seg_sizes,
+                                      uint32_t nseg, uint32_t level, ipls_trace* tr,
+                                      void* stream) {
+  if (nseg == 0 || !h_seg_sizes) return n == 0 ? IPLS_OK : IPLS_ERR_INVALID_ARGUMENT;
+  unsigned __int128 tot = 0;
+  for (uint32_t i = 0; i < nseg; ++i) tot += h_seg_sizes[i];
+  if (tot != n) return IPLS_ERR_INVALID_ARGUMENT;
+  if (n <= 1) return sort_impl(d_keys, n, t, cfg, nullptr, 0, stream, tr);
+  const InitSegs init{h_seg_sizes, nseg, level};
+  return sort_impl(d_keys, n, t, cfg, nullptr, 0, stream, tr, &init);
+}
+
+ipls_status ipls_sort_segments(void* d_keys, size_t n, ipls_key_type t, const ipls_config* cfg,
+                               const uint64_t* h_seg_sizes, uint32_t nseg, uint32_t level,
+                               void* stream) {
+  return sort_segments_impl(d_keys, n, t, cfg, h_seg_sizes, nseg, level, nullptr, stream);
+}
+
+ipls_status ipls_sort_segments_trace(void* d_keys, size_t n, ipls_key_type t,
+                                     const ipls_config* cfg, const uint64_t* h_seg_sizes,
+                                     uint32_t nseg, uint32_t level, ipls_trace* trace,
+                                     void* stream) {
+  if (!trace) return IPLS_ERR_INVALID_ARGUMENT;
+  return sort_segments_impl(d_keys, n, t, cfg, h_seg_sizes, nseg, level, trace, stream);
+}
+
+ipls_status ipls_regroup_runs(const void* d_src, void* d_dst, const uint64_t* h_counts,
+                              uint32_t G, uint32_t nb, void* stream) {
+  if (G == 0 || nb == 0) return IPLS_OK;
+  if (!h_counts || !d_src || !d_dst) return IPLS_ERR_INVALID_ARGUMENT;
+  // run g starts after runs 0..g-1; bucket b of the output after buckets < b (all runs) and
+  // after runs < g's keys of bucket b
+  std::vector<uint64_t> run_start(G + 1, 0), bucket_tot(nb, 0), dst_start(nb + 1, 0);
+  for (uint32_t g = 0; g < G; ++g) {
+    uint64_t t = 0;
+    for (uint32_t b = 0; b < nb; ++b) { t += h_counts[(size_t)g * nb + b]; bucket_tot[b] += h_counts[(size_t)g * nb + b]; }
+    run_start[g + 1] = run_start[g] + t;
+  }
+  for (uint32_t b = 0; b < nb; ++b) dst_start[b + 1] = dst_start[b] + bucket_tot[b];
+  std::vector<Piece> pcs;
+  std::vector<uint64_t> fill(nb, 0);
+  for (uint32_t g = 0; g < G; ++g) {
+    uint64_t so = run_start[g];
+    for (uint32_t b = 0; b < nb; ++b) {
+      const uint64_t c = h_counts[(size_t)g * nb + b];
+      if (c) pcs.push_back(Piece{so, dst_start[b] + fill[b], c});
+      so += c;
+      fill[b] += c;
+    }
+  }
+  if (pcs.empty()) return IPLS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  try {
+    Piece* dp = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&dp), pcs.size() * sizeof(Piece), st));
+    ck(cudaMemcpyAsync(dp, pcs.data(), pcs.size() * sizeof(Piece), cudaMemcpyHostToDevice, st));
+    const uint32_t np = (uint32_t)pcs.size();
+    k_move_pieces<<<std::min<uint32_t>((np + 7) / 8, num_sms() * 8), 256, 0, st>>>(
+        static_cast<const uint64_t*>(d_src), static_cast<uint64_t*>(d_dst), dp, np);
+    ck_launch();
+    ck(cudaFreeAsync(dp, st));
+    ck(cudaStreamSynchronize(st));
+    return IPLS_OK;
+  } catch (const CudaFail& f) {
+    g_last_cuda_error = cudaGetErrorString(f.e);
+    return f.e == cudaErrorMemoryAllocation ? IPLS_ERR_OUT_OF_MEMORY : IPLS_ERR_CUDA;
+  }
 }
 
 size_t ipls_workspace_bytes(size_t n, ipls_key_type t, const ipls_config* cfg) {
@@ -876,6 +1067,7 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
     LevelArgs la{};
     la.src = static_cast<const uint64_t*>(d_in); la.segs = dseg; la.chunks = dch;
     la.models = dmod; la.k = k; la.base_case = 0; la.level = 0; la.chunk_keys = ck_keys; la.nkeys = n;
+    la.dstbuf = 1;
     la.ticket = &dctr->ticket;
     la.status = at<uint64_t>(meta, ML.status);
     la.cflag = at<uint8_t>(meta, ML.cflag);

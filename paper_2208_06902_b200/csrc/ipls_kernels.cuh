@@ -685,6 +685,7 @@ struct LevelArgs {
   const ModelDev* models;
   uint32_t k, base_case, level, chunk_keys;
   uint64_t nkeys;        // length of the arrays (src and both destinations)
+  uint32_t dstbuf;       // buffer the level scatters into: 1 = scratch, 0 = user array
   uint32_t* ticket;
   uint64_t* status;      // [chunk][k]: epoch<<48 | state<<46 | count
   uint32_t* chunk_pre;   // [chunk][k] exclusive prefix within the segment
@@ -892,7 +893,7 @@ __device__ void segment_bases(const LevelArgs& a, uint32_t s, const SegDesc& sg,
 #pragma unroll
   for (int q = 0; q < kCBpt; ++q) x += tot[q];
   uint32_t ex = block_exclusive_scan<kCThreads>(x, os.warp, nullptr);
-  const uint32_t dstbuf = (a.level + 1) & 1;  // 1 = scratch, 0 = user array
+  const uint32_t dstbuf = a.dstbuf;  // 1 = scratch, 0 = user array
 #pragma unroll
   for (int q = 0; q < kCBpt; ++q) {
     const uint32_t b = threadIdx.x * kCBpt + q;
@@ -962,7 +963,7 @@ __device__ void segment_emit(const LevelArgs& a, uint32_t s, const SegDesc& sg, 
   for (int q = 0; q < BPT; ++q)
     if (md.kind != kModelEq3 && bb[q] < k && tot[q] == sg.m) st = 1;  // R10, R24
   const bool stuck = __syncthreads_or(st) != 0;
-  const uint32_t dstbuf = (a.level + 1) & 1;  // 1 = scratch, 0 = user array
+  const uint32_t dstbuf = a.dstbuf;  // 1 = scratch, 0 = user array
   uint32_t cls[BPT];
 #pragma unroll
   for (int q = 0; q < BPT; ++q) {
@@ -2432,6 +2433,31 @@ __global__ void k_snapshot(const SegDesc* __restrict__ segs, const uint64_t* __r
   const SegDesc sg = segs[blockIdx.x];
   const uint64_t* s = (dstbuf ? scr : user) + sg.begin;
   for (uint32_t i = threadIdx.x; i < sg.m; i += blockDim.x) snap[sg.begin + i] = s[i];
+}
+
+// ipls_regroup_runs: move pieces (src offset, dst offset, length) of keys, one warp per piece,
+// coalesced (the multi-GPU exchange's G received runs into bucket-major order).
+struct Piece {
+  uint64_t src, dst;
+  uint64_t len;
+};
+__global__ void k_move_pieces(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+                              const Piece* __restrict__ pieces, uint32_t npieces) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < npieces;
+       w += (gridDim.x * blockDim.x) >> 5) {
+    const Piece pc = pieces[w];
+    for (uint64_t i = lane; i < pc.len; i += 32) dst[pc.dst + i] = __ldcs(src + pc.src + i);
+  }
+}
+
+// ipls_sort_segments (f64): any NaN rejects the input before anything is written (R0).
+__global__ void k_nan_scan(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ err) {
+  int nan = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    nan |= isnan(__longlong_as_double((long long)__ldcs(keys + i)));
+  if (__syncthreads_or(nan) && threadIdx.x == 0) atomicOr(err, kErrNan);
 }
 
 __global__ void k_keys_to_ok(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,

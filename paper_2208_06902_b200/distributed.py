@@ -15,8 +15,16 @@ sort.  A global array is the concatenation, in rank order, of every rank's shard
 4. plan — the per-rank bucket counts are all-gathered; `ipls_assign_ranges` gives rank r the
    contiguous buckets [bounds[r], bounds[r+1]) balanced by count (buckets are range-ordered,
    so contiguous bucket ranges are key ranges);
-5. exchange + finish — one all-to-all moves every bucket range to its rank, and each rank
-   sorts what it received (`ipls_sort_ex`, the single-GPU path).
+5. exchange + finish — one all-to-all moves every bucket range to its rank; the rank puts
+   the G runs it received (one per source, each bucket-major) into bucket-major order
+   (`ipls_regroup_runs`) and resumes the recursion at level 1 with its buckets as the
+   segments (`ipls_sort_segments`): the top level is not repeated, and every model below it
+   is the one a one-GPU sort of the concatenation fits (the regrouped bucket is exactly the
+   stable level-0 child of the global array).
+
+Failures agree: every rank all-reduces (MAX) its status before each collective that follows
+a step that can fail (fit, partition, the receive allocation) and after the local sort, and
+all ranks raise together.
 
 Rank r then holds the r-th key range sorted; the concatenation over ranks is the sorted
 global array.  Every step that touches keys runs in libipls.so's kernels; this module only
@@ -33,7 +41,7 @@ from typing import List, Optional
 import numpy as np
 
 from . import (DEFAULT_SEED, IPLSError, Model, assign_ranges, fit_fmcd, partition_level,
-               sample_size, sample_strata, sort, _key_type_of)
+               regroup_runs, sample_size, sample_strata, sort, sort_segments, _key_type_of)
 
 
 class CudaOps:
@@ -68,6 +76,26 @@ class CudaOps:
         out = torch.empty_like(keys)
         off, _ = partition_level(keys, out, model, key_type=key_type, stream=self.stream)
         return out, [int(x) for x in off.cpu().tolist()]
+
+    def regroup(self, runs, counts: np.ndarray):
+        """The G received runs (counts: G x nb) into bucket-major order (ipls_regroup_runs)."""
+        import torch
+        if counts.shape[0] <= 1:
+            return runs  # one run is bucket-major already
+        out = torch.empty_like(runs)
+        regroup_runs(runs, out, counts, stream=self.stream)
+        return out
+
+    def sort_segments(self, keys, key_type: int, k: int, base_case: int, seed: int, sizes,
+                      level: int) -> int:
+        """Sort range-ordered segments from `level` on (ipls_sort_segments); returns the
+        status instead of raising (see sort)."""
+        try:
+            sort_segments(keys, sizes, level=level, k=k, base_case=base_case, seed=seed,
+                          key_type=key_type, stream=self.stream)
+            return 0
+        except IPLSError as e:
+            return e.status
 
 
 @dataclass
@@ -123,19 +151,41 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
     gbegin, gm = int(sizes[:r].sum()), int(sizes.sum())
     S = sample_size(gm, k) if gm >= 2 else 0
 
-    status = 0
+    def agree(st: int) -> int:
+        t = torch.tensor([st], dtype=torch.int64, device=cdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return int(t.item())
+
+    def attempt(fn):
+        """Run fn; (result, 0) or (None, status) on an IPLSError or a device allocation
+        failure, so that the ranks can agree before the next collective."""
+        try:
+            return fn(), 0
+        except IPLSError as e:
+            return None, e.status
+        except torch.cuda.OutOfMemoryError:
+            return None, 4  # IPLS_ERR_OUT_OF_MEMORY
+
     model: Optional[Model] = None
+    status = 0
     if S >= 4:
-        smp = ops.sample(keys, gbegin, gm, S, seed)               # step 1
+        smp, status = attempt(lambda: ops.sample(keys, gbegin, gm, S, seed))  # step 1
+        st = agree(status)
+        if st:
+            raise IPLSError(st, "in the distributed sample")
         smp_c = smp.to(cdev)
         dist.all_reduce(smp_c, op=dist.ReduceOp.SUM, group=group)
         smp = smp_c.to(dev)
-        model = ops.fit(smp, kt, k)                               # step 2 (same on all ranks)
+        model, status = attempt(lambda: ops.fit(smp, kt, k))          # step 2 (same on all ranks)
     mark("sample+fit")
-    if model is not None:
-        part, off = ops.partition(keys, model, kt)               # step 3
-    else:                                                         # global n < 8
+    if model is not None and status == 0:
+        po, status = attempt(lambda: ops.partition(keys, model, kt))  # step 3
+        part, off = po if po is not None else (keys, [0, keys.numel()])
+    else:                                                         # global n < 8 (or failed)
         part, off = keys, [0, keys.numel()]
+    st = agree(status)
+    if st:
+        raise IPLSError(st, "in the distributed partition")
     part_w = part.view(torch.int64)
     ke = len(off) - 1
     cnt = _all_gather_int64([off[b + 1] - off[b] for b in range(ke)], group, cdev)
@@ -144,18 +194,27 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
     bounds = assign_ranges(total, G)                              # step 4
     send = [off[bounds[d + 1]] - off[bounds[d]] for d in range(G)]
     recv = [int(cnt[s, bounds[r]:bounds[r + 1]].sum()) for s in range(G)]
-    out_w = torch.empty(sum(recv), dtype=torch.int64, device=cdev)  # step 5
-    dist.all_to_all_single(out_w, part_w.to(cdev), output_split_sizes=recv,
+    out_w, status = attempt(lambda: torch.empty(sum(recv), dtype=torch.int64, device=cdev))
+    if status == 0 and sum(recv) > 0xFFFFFFFF:
+        status = 1  # IPLS_ERR_INVALID_ARGUMENT: beyond the ABI's 2^32 - 1 keys per call
+    st = agree(status)
+    if st:
+        raise IPLSError(st, "before the exchange")
+    dist.all_to_all_single(out_w, part_w.to(cdev), output_split_sizes=recv,   # step 5
                            input_split_sizes=send, group=group)
-    out = out_w.to(dev).view(keys.dtype)
+    runs = out_w.to(dev).view(keys.dtype)
     mark("plan+exchange")
+    mine = cnt[:, bounds[r]:bounds[r + 1]]                        # G x (my buckets)
+    out, status = attempt(lambda: ops.regroup(runs, mine))
     if status == 0:
-        status = ops.sort(out, kt, k, base_case, seed)
+        sizes = mine.sum(axis=0)
+        status = ops.sort_segments(out, kt, k, base_case, seed, sizes, 1)
+    else:
+        out = runs
     mark("local sort")
-    st = torch.tensor([status], dtype=torch.int64, device=cdev)
-    dist.all_reduce(st, op=dist.ReduceOp.MAX, group=group)
-    if int(st.item()) != 0:
-        raise IPLSError(int(st.item()), "in the distributed sort")
+    st = agree(status)
+    if st:
+        raise IPLSError(st, "in the distributed sort")
     below = int(sum(cnt[:, :bounds[r]].sum(axis=1))) if bounds[r] > 0 else 0
     return DistResult(out, bounds, model, total, below, gm)
 

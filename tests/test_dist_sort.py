@@ -76,6 +76,24 @@ class OracleOps:
         out, off, _ = oracle.partition(a, m.a, m.b, m.k, m.kind, m.pivot_ok)
         return torch.from_numpy(out.view(np.int64).copy()), [int(x) for x in off]
 
+    def regroup(self, runs, counts):
+        """Bucket-major order of the G received runs (the reference for ipls_regroup_runs)."""
+        bits = runs.view(torch.int64).numpy()
+        pieces, o = [[] for _ in range(counts.shape[1])], 0
+        for g in range(counts.shape[0]):
+            for b in range(counts.shape[1]):
+                c = int(counts[g, b])
+                pieces[b].append(bits[o:o + c])
+                o += c
+        flat = [x for p in pieces for x in p]
+        out = np.concatenate(flat) if flat else bits[:0]
+        return torch.from_numpy(out.copy()).view(runs.dtype)
+
+    def sort_segments(self, t, kt, k, base_case, seed, sizes, level):
+        # the segments are range-ordered: sorting the whole range sorts each of them
+        assert int(np.sum(sizes)) == t.numel()
+        return self.sort(t, kt, k, base_case, seed)
+
 
 def _shards(kind, n, G, seed):
     rng = np.random.default_rng(seed)

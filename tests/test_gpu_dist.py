@@ -135,3 +135,131 @@ def test_fit_sample_unsorted_equals_oracle_fit(ipls, S, k, kind):
         assert m.pivot_ok == int(oracle.ordering_keys(s[S // 2:S // 2 + 1])[0])
     else:
         assert (m.a, m.b, m.D, bool(m.capped)) == (f.A, f.B, f.D, f.capped)
+
+
+# ---------------------------------------------------------------- local sort after exchange --
+def _ok_sorted(a):
+    return a[np.argsort(oracle.ordering_keys(a), kind="stable")]
+
+
+@pytest.mark.parametrize("G,nb", [(1, 5), (2, 1), (3, 7), (5, 64)])
+def test_regroup_runs_is_bucket_major(ipls, G, nb):
+    rng = np.random.default_rng(G * 100 + nb)
+    counts = rng.integers(0, 50, (G, nb)).astype(np.uint64)
+    counts[0, 0] = 0
+    tot = int(counts.sum())
+    src = rng.integers(0, 2 ** 63, tot).astype(np.int64)
+    want, pieces, o = [], [[] for _ in range(nb)], 0
+    for g in range(G):
+        for b in range(nb):
+            c = int(counts[g, b])
+            pieces[b].append(src[o:o + c])
+            o += c
+    want = np.concatenate([x for p in pieces for x in p]) if tot else src
+    s = torch.from_numpy(src).cuda()
+    d = torch.empty_like(s)
+    ipls.regroup_runs(s, d, counts)
+    assert np.array_equal(d.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("name,n", [("C2", 3_000_000), ("C3", 2_000_000), ("C4", 1_000_000)])
+def test_sort_segments_resumes_the_one_gpu_sort(ipls, name, n):
+    """ipls_sort_segments on the stable level-0 partition of an array, with the level-0 buckets
+    as segments, performs exactly the levels >= 1 of the one-GPU sort: every record of the
+    resumed sort equals the oracle's record of the same (level, begin), and the output is the
+    sorted input (the multi-GPU local sort)."""
+    cfg = datagen.CONFIGS[name]
+    a = datagen.generate(name, n)
+    ores = oracle.sort(a.copy(), k=cfg.k, base_case=cfg.base_case, trace=True)
+    r0 = ores.records[0]
+    assert r0.level == 0
+    kt = 0 if a.dtype == np.float64 else 1
+    mdl = ipls.Model(r0.A, r0.B, r0.k_eff, r0.D, r0.kind, r0.capped, r0.pivot_ok)
+    part = torch.empty(n, dtype=torch.int64, device="cuda")
+    off, _ = ipls.partition_level(dev(a), part, mdl, key_type=kt)
+    sizes = np.diff(off.cpu().numpy().astype(np.int64))
+    tr = ipls.sort_trace(part, k=cfg.k, base_case=cfg.base_case, key_type=kt,
+                         segments=sizes, level=1)
+    assert part.cpu().numpy().view(a.dtype).tobytes() == _ok_sorted(a).tobytes()
+    # the oracle's records below level 0, except children it classed homogeneous-final (the
+    # resumed sort cannot know they are one-valued and partitions them once more, EQ3)
+    want = {(o.level, o.begin): o for o in ores.records if o.level >= 1}
+    got = {(g.level, g.begin): g for g in tr.records}
+    for key, o in want.items():
+        g = got[key]
+        assert (g.m, g.S, g.kind, g.D, g.capped, g.pivot_ok) == (o.m, o.S, o.kind, o.D, o.capped, o.pivot_ok)
+        assert g.A == o.A and g.B == o.B
+        assert np.array_equal(g.counts, o.counts)
+    for key, g in got.items():
+        if key not in want:  # only one-valued segments may be extra
+            assert g.kind == ipls.MODEL_EQ3 and g.counts[1] == g.m
+
+
+@pytest.mark.parametrize("kind", ["normal", "dups", "small_segments", "u64"])
+def test_sort_segments_edge_cases(ipls, kind):
+    rng = np.random.default_rng(len(kind))
+    n = 400_000
+    if kind == "u64":
+        a = np.sort(rng.integers(0, 2 ** 64 - 1, n, dtype=np.uint64, endpoint=True))
+    elif kind == "dups":
+        a = np.sort(rng.integers(0, 20, n).astype(np.float64))
+    else:
+        a = np.sort(rng.normal(0, 1, n))
+    if kind == "small_segments":
+        cuts = np.sort(rng.integers(0, n, 3000))  # mostly base-case segments, zeros included
+    else:
+        cuts = np.sort(rng.integers(0, n, 40))
+    cuts = np.concatenate([[0], cuts, cuts[:3], [n]])
+    cuts.sort()
+    sizes = np.diff(cuts)
+    b = a.copy()
+    for lo, hi in zip(cuts[:-1], cuts[1:]):  # shuffle inside each range-ordered segment
+        rng.shuffle(b[lo:hi])
+    t = dev(b)
+    ipls.sort_segments(t, sizes, level=1, k=256, base_case=4096,
+                       key_type=1 if kind == "u64" else 0)
+    assert t.cpu().numpy().view(a.dtype).tobytes() == a.tobytes()
+
+
+def test_sort_segments_nan_leaves_array_unmodified(ipls):
+    a = np.sort(np.random.default_rng(5).normal(0, 1, 100_000))
+    a[77_777] = np.nan
+    t = dev(a)
+    with pytest.raises(ipls.IPLSError) as e:
+        ipls.sort_segments(t, [50_000, 50_000], level=1, k=1024, base_case=4096, key_type=0)
+    assert e.value.status == 2
+    assert t.cpu().numpy().tobytes() == a.tobytes()
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_simulated_ranks_data_path(ipls, G):
+    """The N-rank data path of dist_sort on one GPU (no rank waits on another): the global
+    level-0 model, every shard's stable partition, the exchange as slicing, regroup and the
+    resumed local sorts; the concatenation is the sorted input."""
+    a = datagen.generate("C5", 2_000_000)
+    n = a.size
+    cfg = datagen.CONFIGS["C5"]
+    r0 = oracle.sort(a.copy(), k=cfg.k, base_case=cfg.base_case, trace=True).records[0]
+    mdl = ipls.Model(r0.A, r0.B, r0.k_eff, r0.D, r0.kind, r0.capped, r0.pivot_ok)
+    shards = np.array_split(a, G)
+    parts, offs = [], []
+    for sh in shards:
+        p = torch.empty(sh.size, dtype=torch.int64, device="cuda")
+        off, _ = ipls.partition_level(dev(sh), p, mdl, key_type=0)
+        parts.append(p)
+        offs.append(off.cpu().numpy().astype(np.int64))
+    cnt = np.stack([np.diff(o) for o in offs])
+    bounds = ipls.assign_ranges(cnt.sum(axis=0), G)
+    out = []
+    for r in range(G):
+        b0, b1 = bounds[r], bounds[r + 1]
+        runs = torch.cat([parts[s][int(offs[s][b0]):int(offs[s][b1])] for s in range(G)])
+        mine = cnt[:, b0:b1].astype(np.uint64)
+        reg = torch.empty_like(runs)
+        if runs.numel():
+            ipls.regroup_runs(runs, reg, mine)
+            ipls.sort_segments(reg, mine.sum(axis=0), level=1, k=cfg.k, base_case=cfg.base_case,
+                               key_type=0)
+        out.append(reg.cpu().numpy())
+    got = np.concatenate(out).view(np.float64)
+    assert got.tobytes() == _ok_sorted(a).tobytes()
