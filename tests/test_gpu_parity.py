@@ -566,3 +566,52 @@ def test_match_rank_path_keeps_stable_layouts(ipls, kind):
         sort_parity_with_layouts(ipls, a, 1024, 1000)
     finally:
         ipls.lib().ipls_debug_force_match_rank(0)
+
+
+@pytest.mark.parametrize("n,k", [(100_000, 256), (1_000_000, 1024)])
+def test_no_progress_guard_fires_and_matches_oracle(ipls, n, k):
+    """The no-progress guard (R10): a model that keeps all m keys of a segment in one bucket
+    re-queues the segment with a forced equality split.  With FMCD it cannot fire on a
+    segment's own sample (the anchors s[D] and s[N-1-D] land k-2 buckets apart, DESIGN.md
+    R10), but IPS4o's splitter tree can: on a one-valued root every splitter equals the key,
+    every key descends to leaf 0.  The GPU must re-queue exactly as the oracle does."""
+    a = np.full(n, 3.25)
+    want = a.copy()
+    ores = oracle.sort(want, k=k, base_case=4096, trace=True, model=oracle.MODEL_TREE)
+    t = dev(a)
+    gtr = ipls.sort_trace(t, k=k, base_case=4096, key_type=0, model=ipls.MODEL_TREE)
+    assert host(t, np.float64).tobytes() == want.tobytes()
+    compare_traces(gtr, ores)
+    assert any(r.requeued for r in gtr.records)
+    assert any(r.level == 1 and r.kind == ipls.MODEL_EQ3 for r in gtr.records)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_configs_full_size_layout_after_every_level(ipls, name):
+    """Full BASELINE sizes: the array image after every level against the oracle's
+    (tests/golden/oracle_layouts.txt, written by make_oracle_layouts.py from the oracle only),
+    element by element outside the children of terminal segments and as a multiset inside
+    each of them (their interior order is unspecified, R11)."""
+    import sys
+    sys.path.insert(0, GOLD)
+    from make_oracle_layouts import free_ranges, layout_digest
+    want = {}
+    with open(os.path.join(GOLD, "oracle_layouts.txt")) as f:
+        for line in f:
+            tok = line.split()
+            if tok and tok[0] == "LAYOUT":
+                want.setdefault(tok[1], {})[int(tok[2])] = tok[3]
+    cfg = datagen.CONFIGS[name]
+    a = datagen.generate(name)
+    t = dev(a)
+    del a
+    levels = len(want[name])
+    gtr = ipls.sort_trace(t, k=cfg.k, base_case=cfg.base_case,
+                          key_type=kt_of(datagen.generate(name, 1)), snapshot_levels=levels)
+    assert gtr.levels == levels
+    for lv in range(levels):
+        img = gtr.snapshots[lv].cpu().numpy().view(np.uint64)
+        lo, hi = free_ranges(gtr.records, lv, cfg.base_case)
+        assert layout_digest(img, lo, hi) == want[name][lv], f"{name}: layout after level {lv}"
+    del gtr
+    torch.cuda.empty_cache()
