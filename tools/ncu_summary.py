@@ -5,7 +5,10 @@ METRICS = [
     ("gpu__time_duration.sum", "time"),
     ("dram__bytes_read.sum", "dram_rd"),
     ("dram__bytes_write.sum", "dram_wr"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram_%"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_%"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "lsu_wf_%"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem_wf"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_%"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_%"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps_act_%"),
     ("smsp__inst_executed.sum", "warp_inst"),

@@ -3,8 +3,12 @@ profiles/ (read by bench.py for roofline.traffic).  usage: traffic_json.py REPOR
 import csv, io, json, re, subprocess, sys
 from collections import defaultdict
 
-FAMILY = {"k_scatter": "scatter", "k_base_warp": "base_warp", "k_classify_scan": "classify_scan",
-          "k_base_sort": "base_sort", "k_gather_fit": "gather_fit", "k_fit_small": "fit_small"}
+# the library's profile scope "scatter" brackets a level's two scatter kernels (stable, then
+# terminal): their traffic is summed per level
+FAMILY = {"k_scatter_stable": "scatter", "k_scatter_term": "scatter", "k_base_warp": "base_warp",
+          "k_classify_scan": "classify_scan", "k_base_sort": "base_sort",
+          "k_gather_fit": "gather_fit", "k_fit_small": "fit_small", "k_emit": "emit",
+          "k_fill": "fill"}
 
 
 def main(rep, note):
@@ -21,7 +25,11 @@ def main(rep, note):
             continue
         rd = float(r[iR]) * scale[units[iR]]
         wr = float(r[iW]) * scale[units[iW]]
-        per[fam].append([int(rd), int(wr)])
+        if "k_scatter_term" in r[iK] and per[fam]:
+            per[fam][-1][0] += int(rd)
+            per[fam][-1][1] += int(wr)
+        else:
+            per[fam].append([int(rd), int(wr)])
     res = {"source": note, "kernels": {}}
     for fam, l in per.items():
         res["kernels"][fam] = {"dram_bytes_per_launch": int(sum(a + b for a, b in l) / len(l)),
