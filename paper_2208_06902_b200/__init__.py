@@ -85,7 +85,7 @@ SYMBOLS = ["ipls_default_config", "ipls_sort_f64", "ipls_sort_u64", "ipls_sort_e
            "ipls_kernel_launch_count", "ipls_profile_enable", "ipls_profile_reset",
            "ipls_profile_read", "ipls_sample_size", "ipls_sample_strata", "ipls_assign_ranges", "ipls_fit_sample", "ipls_debug_set_epoch",
            "ipls_debug_force_match_rank", "ipls_sort_segments",
-           "ipls_regroup_runs", "ipls_sort_segments_trace"]
+           "ipls_regroup_runs", "ipls_sort_segments_trace", "ipls_debug_term_mode"]
 
 _lib = None
 
@@ -123,6 +123,7 @@ def lib():
         L.ipls_profile_read.restype = sz
         L.ipls_debug_set_epoch.argtypes = [u32]; L.ipls_debug_set_epoch.restype = None
         L.ipls_debug_force_match_rank.argtypes = [i32]; L.ipls_debug_force_match_rank.restype = None
+        L.ipls_debug_term_mode.argtypes = [i32]; L.ipls_debug_term_mode.restype = None
         L.ipls_fit_sample.argtypes = [vp, sz, i32, u32, ctypes.POINTER(_Model), vp]
         L.ipls_fit_sample.restype = i32
         L.ipls_sample_size.argtypes = [u64, u32]; L.ipls_sample_size.restype = u32

@@ -26,6 +26,7 @@ using namespace ipls;
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_term_mode{0};  // ipls_debug_term_mode: 0 auto, 1 always fused, 2 never
 thread_local std::string g_last_cuda_error;
 
 struct CudaFail {
@@ -101,6 +102,12 @@ void prof_collect() {
     t_event_pool.push_back(p.e1);
   }
   t_pending.clear();
+}
+// algorithmic bytes known only after a level (the base case inside k_term_fused)
+void prof_add_bytes(const char* name, double bytes) {
+  if (!g_prof_on.load() || bytes == 0.0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof[name].bytes += bytes;
 }
 #define IPLS_CAT2(a, b) a##b
 #define IPLS_CAT(a, b) IPLS_CAT2(a, b)
@@ -181,7 +188,7 @@ FixedLayout fixed_layout(const Params& p) {
 // Per-level metadata (sized by the level's actual counts).  `status` comes first so a fresh
 // allocation can be cleared cheaply.
 struct MetaLayout {
-  size_t status, cflag, cref, chunk_pre, models, samples, seg_dst, seg_tot, seg_term,
+  size_t status, cflag, cref, chunk_pre, models, samples, seg_dst, seg_tot, seg_term, seg_done,
       tree, total;
 };
 
@@ -199,6 +206,7 @@ MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_
   L.seg_dst = take(segs * k * 8);
   L.seg_tot = take(segs * k * 4);
   L.seg_term = take(segs * 4);
+  L.seg_done = take(segs * 4);
   L.tree = take(tree ? segs * kMaxK * 8 : 0);  // splitter heaps (8 KB per segment)
   L.total = o;
   return L;
@@ -270,6 +278,7 @@ struct TraceSink {
 size_t scatter_stable_smem(uint32_t k) { return scatter_stable_smem_bytes(k); }
 size_t scatter_term_smem(uint32_t k) { return scatter_term_smem_bytes(k); }
 
+uint32_t num_sms();
 // Both scatter kernels over the level's chunks: each one takes its own kind of chunk (stable
 // or terminal, known on the device after K2) and returns at once for the other.
 template <bool F64>
@@ -284,6 +293,17 @@ void launch_scatter(uint32_t nchunk, cudaStream_t st, const LevelArgs& la, uint6
   ck_launch();
   }
   if (stable_only) return;
+  if (la.fused_term) {
+    // terminal chunks, each terminal segment base-sorted by the CTA that completes it
+    IPLS_PROF("term_fused", 0);
+    const uint32_t grid = std::min(nchunk, num_sms());
+    if (tree)
+      k_term_fused<F64, true><<<grid, kTThreads, fused_smem_bytes(la.k), st>>>(la, user, scr, nchunk);
+    else
+      k_term_fused<F64, false><<<grid, kTThreads, fused_smem_bytes(la.k), st>>>(la, user, scr, nchunk);
+    ck_launch();
+    return;
+  }
   IPLS_PROF("scatter_term", 0);
   if (tree)
     k_scatter_term<F64, true><<<nchunk, kTThreads, scatter_term_smem(la.k), st>>>(la, user, scr);
@@ -350,6 +370,9 @@ void set_attrs() {
     ck(cudaFuncSetAttribute(tr ? k_scatter_term<F64, true> : k_scatter_term<F64, false>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)scatter_term_smem(kMaxK)));
+    ck(cudaFuncSetAttribute(tr ? k_term_fused<F64, true> : k_term_fused<F64, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)fused_smem_bytes(kMaxK)));
     ck(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)win_scratch_bytes(kMaxK)));
   }
@@ -553,6 +576,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     // per level; the epoch tag still orders the words written within the level.
     (void)wrapped;
     ck(cudaMemsetAsync(at<uint64_t>(meta, ML.status), 0, (size_t)nchunk * k * 8, st));
+    ck(cudaMemsetAsync(at<uint32_t>(meta, ML.seg_done), 0, (size_t)nseg * 4, st));
     ModelDev* models = at<ModelDev>(meta, ML.models);
     uint64_t* samples = at<uint64_t>(meta, ML.samples);
     uint64_t* seg_dst = at<uint64_t>(meta, ML.seg_dst);
@@ -588,11 +612,19 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     la.src = src; la.segs = segs; la.chunks = chunks; la.models = models;
     la.k = k; la.base_case = p.B; la.level = level; la.chunk_keys = p.chunk_keys; la.nkeys = n;
     la.dstbuf = (iter + 1) & 1;
+    // Fusing the last level with the base case pays when a terminal segment is worth a CTA's
+    // base-case pass (its packing runs inside the completing CTA): levels whose segments
+    // average >= 32 Ki keys (C2-C5 level 1); small segments (level 2 of C3/C5) keep the
+    // separate kernels, whose emit runs 4 CTAs per SM.
+    la.fused_term = (level_keys / std::max<uint32_t>(nseg, 1) >= 32768u) ? 1u : 0u;
+    if (g_term_mode.load() == 1) la.fused_term = 1;
+    if (g_term_mode.load() == 2) la.fused_term = 0;
     la.ticket = &cctr->ticket;
     la.status = at<uint64_t>(meta, ML.status);
     la.cflag = at<uint8_t>(meta, ML.cflag);
     la.cref = at<uint64_t>(meta, ML.cref);
     la.seg_term = at<uint32_t>(meta, ML.seg_term);
+    la.seg_done = at<uint32_t>(meta, ML.seg_done);
     la.chunk_pre = chunk_pre;
     la.seg_dst = seg_dst;
     la.seg_tot = seg_tot;
@@ -663,6 +695,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     ck(cudaStreamSynchronize(st));
     const LevelCounters c = h_ctr[0];
     const uint32_t herr = h_ctr[1].err;
+    prof_add_bytes("scatter", 16.0 * c.term_keys);  // the base case done inside k_term_fused
     if (herr & kErrNan) return IPLS_ERR_NAN_KEY;
     if (herr & kErrOverflow) return IPLS_ERR_OUT_OF_MEMORY;
 
@@ -1116,6 +1149,8 @@ const char* ipls_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
 uint64_t ipls_kernel_launch_count(void) { return g_launches.load(); }
 
 void ipls_debug_set_epoch(uint32_t e) { g_epoch.store(e); }
+
+void ipls_debug_term_mode(int mode) { g_term_mode.store(mode); }
 
 void ipls_debug_force_match_rank(int on) {
   const int v = on ? 1 : 0;

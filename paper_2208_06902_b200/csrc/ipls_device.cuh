@@ -61,7 +61,9 @@ struct LevelCounters {      // device-side counters of the level being built
   uint64_t win_keys;        // keys in this level's small base-case windows
   uint64_t wbig_keys;       // keys in this level's big base-case windows
   uint64_t fill_keys;       // keys in this level's fills
-  uint32_t n_redo, pad2;    // this level's segments k_fit_small left to k_gather_fit
+  uint32_t n_redo;          // this level's segments k_fit_small left to k_gather_fit
+  uint32_t sticket;         // chunk tickets of k_term_fused (next level's struct, zeroed)
+  uint64_t term_keys;       // keys base-sorted inside k_term_fused
 };
 
 constexpr uint32_t kErrNan = 1u;

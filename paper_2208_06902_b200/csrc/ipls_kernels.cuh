@@ -686,6 +686,7 @@ struct LevelArgs {
   uint32_t k, base_case, level, chunk_keys;
   uint64_t nkeys;        // length of the arrays (src and both destinations)
   uint32_t dstbuf;       // buffer the level scatters into: 1 = scratch, 0 = user array
+  uint32_t fused_term;   // terminal segments go through k_term_fused (else k_scatter_term)
   uint32_t* ticket;
   uint64_t* status;      // [chunk][k]: epoch<<48 | state<<46 | count
   uint32_t* chunk_pre;   // [chunk][k] exclusive prefix within the segment
@@ -694,6 +695,7 @@ struct LevelArgs {
   uint8_t* cflag;        // [chunk][k] scatter homogeneity flag: 0 empty, 1 one value, 2 several
   uint64_t* cref;        // [chunk][k] the chunk's value of a one-value bucket
   uint32_t* seg_term;    // [seg]      1: every child <= base case (terminal segment)
+  uint32_t* seg_done;    // [seg]      chunks of the segment scattered (k_term_fused)
   uint32_t epoch;
   uint32_t* err;
   int check_nan;
@@ -1769,6 +1771,7 @@ __global__ __launch_bounds__(kEThreads) void k_emit(LevelArgs a) {
   __shared__ OffSmem os;
   if (*((volatile const uint32_t*)a.err) & kErrNan) return;
   const uint32_t s = blockIdx.x;
+  if (a.fused_term && a.seg_term[s]) return;  // k_term_fused packed and sorted its children
   const SegDesc sg = a.segs[s];
   const ModelDev md = a.models[s];
   segment_emit<kEThreads>(a, s, sg, md, os, reinterpret_cast<uint32_t*>(smraw));
@@ -2159,17 +2162,16 @@ __device__ void warp_bitonic_ok(uint64_t* B, uint32_t len, int lane) {
   __syncwarp();
 }
 
+// One warp sorts the windows first, first + stride, ... < nwin of `wins` (its smem region:
+// IN, bins; its two mbarriers, initialised by the caller; it_base: the number of windows the
+// warp has taken through these mbarriers so far, which fixes their phase).
 template <bool F64>
-__global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
-    const Window* __restrict__ wins, uint32_t nwin, uint64_t* __restrict__ user,
-    const uint64_t* __restrict__ scr) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  __shared__ uint64_t s_mbar[kWBWarps][2];
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  uint64_t* IN = reinterpret_cast<uint64_t*>(smraw + wp * kWBSmemPerWarp);  // 2 x kWBStride
-  uint32_t* bins = reinterpret_cast<uint32_t*>(IN + 2 * kWBStride);          // kWBBinWords
-  uint64_t* mbar = s_mbar[wp];
-  const uint32_t gw = blockIdx.x * kWBWarps + wp, gstride = gridDim.x * kWBWarps;
+__device__ void base_warp_windows(const Window* __restrict__ wins, uint32_t first, uint32_t nwin,
+                                  uint32_t stride, uint64_t* __restrict__ user,
+                                  const uint64_t* __restrict__ scr, uint64_t* IN, uint32_t* bins,
+                                  uint64_t* mbar, uint32_t& it_base) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = first, gstride = stride;
   // lane 0: start the bulk copy of the window described by wv into IN[b].  Descriptors are
   // loaded two windows ahead so that their global latency is off the critical path.
   auto issue = [&](const Window& wv, int b) {
@@ -2182,12 +2184,6 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
       mbar_arrive(&mbar[b]);
     }
   };
-  if (lane == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
 #ifdef IPLS_BASE_TIMING
   long long t_prev_ = clock64();
   unsigned long long acc_[10] = {0};
@@ -2197,10 +2193,11 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
 #endif
   Window d_cur{}, d_nxt{};  // lane 0: descriptors of windows cur and cur+1 (in flight)
   if (lane == 0) {
-    if (gw < nwin) { d_cur = wins[gw]; issue(d_cur, 0); }
+    if (gw < nwin) { d_cur = wins[gw]; issue(d_cur, it_base & 1); }
     if (gw + gstride < nwin) d_nxt = wins[gw + gstride];
   }
-  for (uint32_t it = 0, cur = gw; cur < nwin; ++it, cur += gstride) {
+  uint32_t it = it_base;
+  for (uint32_t cur = gw; cur < nwin; ++it, cur += gstride) {
     const int b = it & 1;
     Window wv;
     wv.begin = __shfl_sync(0xffffffffu, d_cur.begin, 0);
@@ -2414,10 +2411,136 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     fence_proxy_async_smem();  // generic accesses to IN[b] before the bulk copy that reuses it
     __syncwarp();
   }
+  it_base = it;
 #ifdef IPLS_BASE_TIMING
   if (lane == 0)
     for (int q = 0; q < 10; ++q) atomicAdd(&g_base_phase[q], acc_[q]);
 #endif
+}
+
+template <bool F64>
+__global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
+    const Window* __restrict__ wins, uint32_t nwin, uint64_t* __restrict__ user,
+    const uint64_t* __restrict__ scr) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ uint64_t s_mbar[kWBWarps][2];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  uint64_t* IN = reinterpret_cast<uint64_t*>(smraw + wp * kWBSmemPerWarp);  // 2 x kWBStride
+  uint32_t* bins = reinterpret_cast<uint32_t*>(IN + 2 * kWBStride);          // kWBBinWords
+  uint64_t* mbar = s_mbar[wp];
+  if (lane == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t it = 0;
+  base_warp_windows<F64>(wins, blockIdx.x * kWBWarps + wp, nwin, gridDim.x * kWBWarps, user, scr,
+                         IN, bins, mbar, it);
+}
+
+// ------------------------------------------------------------------------------------
+// Last partition level fused with the base case (P:136-142, P:708,
+// P:725).  Persistent CTAs (one per SM, 1024 threads) take the level's terminal chunks by
+// ticket and scatter each one (scatter_term_chunk).  The CTA that completes a segment's last
+// chunk then base-sorts that segment's children itself, right away, while they are still in
+// the L2 (the level's data in flight at any time is ~148 chunks): it packs the children of
+// <= kWBCap keys into windows (pack_windows, into shared memory) and its 32 warps sort them
+// (base_warp_windows, the k_base_warp code); children above kWBCap become windows of
+// k_base_sort, launched after the level.  Terminal segments get no segment_emit (k_emit skips
+// them) and no k_base_warp windows.  Shared memory: the scatter's tile ring, then the base
+// warps' regions plus the segment's window list.
+constexpr size_t kFusedListOff = kWBSmemPerWarp * kWBWarps;  // window list after the warps
+constexpr size_t fused_smem_bytes(uint32_t k) {
+  return (kFusedListOff + (size_t)kMaxK * sizeof(Window)) > scatter_term_smem_bytes(k)
+             ? kFusedListOff + (size_t)kMaxK * sizeof(Window)
+             : scatter_term_smem_bytes(k);
+}
+static_assert(kWBWarps * 32 == kTThreads, "the fused kernel's warps are the base warps");
+constexpr uint32_t kFusedMaxM = 262144;  // larger segments: windows to k_base_warp
+
+template <bool F64, bool TREE>
+__global__ __launch_bounds__(kTThreads, 1) void k_term_fused(LevelArgs a, uint64_t* __restrict__ dst_user,
+                                                             uint64_t* __restrict__ dst_scr,
+                                                             uint32_t nchunk) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ uint64_t s_mbar[kWBWarps][2];
+  __shared__ OffSmem os;
+  __shared__ uint32_t s_ticket, s_last, s_nw;
+  __shared__ uint64_t s_keys;
+  const uint32_t t = threadIdx.x;
+  const int lane = t & 31, wp = t >> 5;
+  uint64_t* IN = reinterpret_cast<uint64_t*>(smraw + wp * kWBSmemPerWarp);
+  uint32_t* bins = reinterpret_cast<uint32_t*>(IN + 2 * kWBStride);
+  Window* list = reinterpret_cast<Window*>(smraw + kFusedListOff);
+  if (lane == 0) {
+    mbar_init(&s_mbar[wp][0], 1);
+    mbar_init(&s_mbar[wp][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t it_base = 0;  // windows this warp has sorted (mbarrier phase)
+  const uint32_t k = a.k;
+  if (*((volatile const uint32_t*)a.err) & kErrNan) return;
+  while (true) {
+    __syncthreads();
+    if (t == 0) s_ticket = atomicAdd(&a.nctr->sticket, 1u);
+    __syncthreads();
+    const uint32_t c = s_ticket;
+    if (c >= nchunk) break;
+    const ChunkDesc ch = a.chunks[c];
+    if (!a.seg_term[ch.seg]) continue;  // k_scatter_stable's chunk
+    ModelDev md = a.models[ch.seg];
+    tree_top_to_smem<TREE, kTThreads>(md, k);
+    constexpr int kMain = TREE ? (int)kModelTree : (int)kModelLinear;
+    if (md.kind == kModelEq3)
+      scatter_term_chunk<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw);
+    else
+      scatter_term_chunk<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
+    // this chunk's stores are visible before it counts; the last one reads them all
+    __threadfence();
+    __syncthreads();
+    const SegDesc sg = a.segs[ch.seg];
+    if (t == 0) s_last = (atomicAdd(&a.seg_done[ch.seg], 1u) == sg.nchunks - 1) ? 1u : 0u;
+    __syncthreads();
+    if (!s_last) continue;
+    __threadfence();
+    // ---- the segment's windows (thread t owns child t) ----
+    const uint32_t b = t;
+    const uint32_t tot = (b < k) ? a.seg_tot[(size_t)ch.seg * k + b] : 0u;
+    const uint32_t base = (b < k) ? (uint32_t)((a.seg_dst[(size_t)ch.seg * k + b] & ~kDstUserBit) - sg.begin) : 0u;
+    const uint32_t dstbuf = a.dstbuf;
+    if (t == 0) { s_nw = 0; s_keys = 0; }
+    __syncthreads();
+    // Once the chunk tickets have run out, the remaining segments complete at the very end
+    // of the kernel; sorting them here would leave most SMs idle behind a few CTAs, so their
+    // windows go to the level's k_base_warp launch instead (all SMs).
+    // Likewise a segment above kFusedMaxM keys: one CTA would hold it long after the others.
+    if (t == 0) s_last = *((volatile const uint32_t*)&a.nctr->sticket) >= nchunk || sg.m > kFusedMaxM;
+    __syncthreads();
+    const bool tail = s_last != 0;  // block-uniform
+    {
+      const uint32_t bb[1] = {b < k ? b : k}, bs[1] = {base}, tt[1] = {tot};
+      const bool small[1] = {b < k && tot > 0 && tot <= (uint32_t)kWBCap};
+      const bool big[1] = {b < k && tot > (uint32_t)kWBCap};
+      if (tail)
+        pack_windows<kTThreads>(a, sg, k, bb, bs, tt, small, (uint32_t)kWBCap, dstbuf, os,
+                                reinterpret_cast<uint32_t*>(smraw), a.wins, a.cap_wins,
+                                &a.nctr->n_windows, &a.nctr->win_keys);
+      else
+        pack_windows<kTThreads>(a, sg, k, bb, bs, tt, small, (uint32_t)kWBCap, dstbuf, os,
+                                reinterpret_cast<uint32_t*>(smraw), list, kMaxK, &s_nw, &s_keys);
+      // children above kWBCap: windows of <= kBigCap keys for k_base_sort, after the level
+      pack_windows<kTThreads>(a, sg, k, bb, bs, tt, big, (uint32_t)kBigCap, dstbuf, os,
+                              reinterpret_cast<uint32_t*>(smraw), a.wins_big, a.cap_wbig,
+                              &a.nctr->n_wbig, &a.nctr->wbig_keys);
+    }
+    if (tail) continue;
+    fence_proxy_async_smem();  // generic accesses (stage, scratch) before the warps' bulk loads
+    __syncthreads();
+    if (t == 0) atomicAdd((unsigned long long*)&a.nctr->term_keys, (unsigned long long)s_keys);
+    base_warp_windows<F64>(list, wp, s_nw, kWBWarps, dst_user, dst_scr, IN, bins, s_mbar[wp], it_base);
+    fence_proxy_async_smem();  // and before the next chunk's tile ring
+  }
 }
 
 __global__ void k_fill(const Fill* __restrict__ fills, uint64_t* __restrict__ user) {

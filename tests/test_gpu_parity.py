@@ -615,3 +615,34 @@ def test_configs_full_size_layout_after_every_level(ipls, name):
         assert layout_digest(img, lo, hi) == want[name][lv], f"{name}: layout after level {lv}"
     del gtr
     torch.cuda.empty_cache()
+
+
+@pytest.fixture(params=[1, 2], ids=["fused", "separate"])
+def term_mode(ipls, request):
+    ipls.lib().ipls_debug_term_mode(request.param)
+    yield request.param
+    ipls.lib().ipls_debug_term_mode(0)
+
+
+@pytest.mark.parametrize("kind", ["normal", "lognormal", "few_distinct", "mixture", "u64_above_2_53"])
+@pytest.mark.parametrize("n,k,B", [(70_001, 256, 4096), (300_000, 1024, 4096), (200_000, 64, 100)])
+def test_terminal_paths_parity(ipls, term_mode, kind, n, k, B):
+    """Both ways of processing a level's terminal segments -- the last level fused with the
+    base case (k_term_fused) and the separate terminal scatter + base-case
+    kernels -- give the oracle's records and layouts after every level and its final array
+    (the size rule that picks one in production is overridden here)."""
+    rng = np.random.default_rng(n + k + len(kind))
+    a = datagen.fuzz_array(rng, n, kind)
+    sort_parity_with_layouts(ipls, a, k, B)
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_terminal_paths_configs_scaled(ipls, term_mode, name):
+    a = datagen.generate(name, 3_000_000)
+    cfg = datagen.CONFIGS[name]
+    want = a.copy()
+    ores = oracle.sort(want, k=cfg.k, base_case=cfg.base_case, trace=True)
+    t = dev(a)
+    gtr = ipls.sort_trace(t, k=cfg.k, base_case=cfg.base_case, key_type=kt_of(a))
+    assert host(t, a.dtype).tobytes() == want.tobytes()
+    compare_traces(gtr, ores)
