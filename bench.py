@@ -282,7 +282,7 @@ def bench_dist(args, world, rank, local):
     torch.cuda.synchronize()
     ipls.profile_enable(False)
     prof = ipls.profile_read()
-    nested = {"scatter_stable", "scatter_term"}
+    nested = {"scatter_stable", "scatter_term", "term_fused"}
     dom = max((k_ for k_ in prof if prof[k_][2] > 0 and k_ not in nested), key=lambda k_: prof[k_][1])
     d_launch, d_ms, d_bytes = prof[dom]
     achieved = d_bytes / (d_ms / 1e3) / 1e9
@@ -473,7 +473,7 @@ def main():
     peak, peak_kind = load_peaks()
     # "scatter" brackets both scatter kernels of a level; scatter_stable / scatter_term are the
     # two kernels inside it (shares are over the top-level entries only)
-    nested = {"scatter_stable", "scatter_term"}
+    nested = {"scatter_stable", "scatter_term", "term_fused"}
     tot_prof_ms = sum(v[1] for k_, v in prof.items() if k_ not in nested)
     dom = max((k_ for k_ in prof if prof[k_][2] > 0 and k_ not in nested), key=lambda k_: prof[k_][1])
     d_launch, d_ms, d_bytes = prof[dom]
