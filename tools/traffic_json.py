@@ -5,7 +5,8 @@ from collections import defaultdict
 
 # the library's profile scope "scatter" brackets a level's two scatter kernels (stable, then
 # terminal): their traffic is summed per level
-FAMILY = {"k_scatter_stable": "scatter", "k_scatter_term": "scatter", "k_base_warp": "base_warp",
+FAMILY = {"k_scatter_stable": "scatter", "k_scatter_term": "scatter", "k_term_fused": "scatter",
+          "k_base_warp": "base_warp",
           "k_classify_scan": "classify_scan", "k_base_sort": "base_sort",
           "k_gather_fit": "gather_fit", "k_fit_small": "fit_small", "k_emit": "emit",
           "k_fill": "fill"}
@@ -25,7 +26,7 @@ def main(rep, note):
             continue
         rd = float(r[iR]) * scale[units[iR]]
         wr = float(r[iW]) * scale[units[iW]]
-        if "k_scatter_term" in r[iK] and per[fam]:
+        if ("k_scatter_term" in r[iK] or "k_term_fused" in r[iK]) and per[fam]:
             per[fam][-1][0] += int(rd)
             per[fam][-1][1] += int(wr)
         else:
