@@ -128,9 +128,11 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
  * the global level-0 sample it holds (ipls_sample_strata) and a SUM all-reduce assembles the
  * whole sample; (2) every rank sorts it (ipls_sort_ex) and fits the same model
  * (ipls_fit_fmcd); (3) every rank partitions its shard by that model (ipls_partition_level);
- * (4) the per-rank bucket counts are all-gathered and ipls_assign_ranges gives rank r the
- * contiguous buckets [bounds[r], bounds[r+1]); (5) one all-to-all moves the keys and every
- * rank sorts what it received (ipls_sort_ex).  Rank r then holds the r-th key range. */
+ * (4) the per-rank bucket counts are all-gathered and ipls_assign_cuts gives rank r the
+ * global positions [cuts[r], cuts[r+1]) of the bucket-major order (bucket boundaries, or
+ * inside EQ3's one-valued ==pivot bucket); (5) one all-to-all moves the keys, every rank puts
+ * its G runs into bucket-major order (ipls_regroup_runs) and resumes the recursion at level 1
+ * (ipls_sort_segments).  Rank r then holds the r-th key range. */
 
 /* Sort n keys that form nseg consecutive range-ordered segments -- every key of segment i
  * precedes (ordering key) every key of segment i+1 -- by resuming the recursion
@@ -181,6 +183,19 @@ ipls_status ipls_sample_strata(const void* d_keys, size_t n_local, uint64_t glob
  * buckets [bounds[r], bounds[r+1]).  Errors: INVALID_ARGUMENT (NULL, k == 0, G == 0). */
 ipls_status ipls_assign_ranges(const uint64_t* h_counts, uint32_t k, uint32_t G,
                                uint32_t* h_bounds);
+
+/* Global cut positions for G ranks when some buckets may be split between ranks (SURVEY
+ * §8(e) step 4; a bucket known to hold one key value, e.g. EQ3's ==pivot bucket (R5), can go
+ * to several ranks without changing the sorted result).  Host only.  h_counts: k global bucket
+ * counts; h_splittable: k flags (NULL = none).  h_cuts: G+1 positions out in the bucket-major
+ * global order; cuts[0] = 0, cuts[G] = total, nondecreasing; cuts[r] is the candidate >=
+ * cuts[r-1] closest to r/G of the total (ties: the lower), the candidates being the bucket
+ * boundaries and every position strictly inside a splittable bucket.  Rank r receives
+ * positions [cuts[r], cuts[r+1]).  With no splittable bucket cuts[r] is the prefix count at
+ * ipls_assign_ranges' bounds[r].  Errors: INVALID_ARGUMENT (NULL counts/cuts, k == 0,
+ * G == 0, total >= 2^64). */
+ipls_status ipls_assign_cuts(const uint64_t* h_counts, uint32_t k, uint32_t G,
+                             const uint8_t* h_splittable, uint64_t* h_cuts);
 
 /* ---- trace (tests and diagnostics) ---- */
 typedef struct {

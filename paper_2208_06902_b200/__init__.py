@@ -18,7 +18,7 @@ import numpy as np
 __all__ = [
     "IPLSError", "lib", "sort", "sort_host", "fit_fmcd", "partition_level", "sort_trace",
     "workspace_bytes", "Model", "Record", "KEY_F64", "KEY_U64", "MODEL_LINEAR", "MODEL_EQ3", "MODEL_TREE",
-    "DEFAULT_SEED", "launch_count", "sample_size", "sample_strata", "assign_ranges",
+    "DEFAULT_SEED", "launch_count", "sample_size", "sample_strata", "assign_ranges", "assign_cuts",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -83,7 +83,7 @@ SYMBOLS = ["ipls_default_config", "ipls_sort_f64", "ipls_sort_u64", "ipls_sort_e
            "ipls_workspace_bytes", "ipls_sort_host", "ipls_fit_fmcd", "ipls_partition_level",
            "ipls_sort_trace", "ipls_status_string", "ipls_last_cuda_error",
            "ipls_kernel_launch_count", "ipls_profile_enable", "ipls_profile_reset",
-           "ipls_profile_read", "ipls_sample_size", "ipls_sample_strata", "ipls_assign_ranges", "ipls_fit_sample", "ipls_debug_set_epoch",
+           "ipls_profile_read", "ipls_sample_size", "ipls_sample_strata", "ipls_assign_ranges", "ipls_assign_cuts", "ipls_fit_sample", "ipls_debug_set_epoch",
            "ipls_debug_force_match_rank", "ipls_sort_segments",
            "ipls_regroup_runs", "ipls_sort_segments_trace", "ipls_debug_term_mode"]
 
@@ -130,6 +130,7 @@ def lib():
         L.ipls_sample_strata.argtypes = [vp, sz, u64, u64, u32, u64, vp, vp]
         L.ipls_sample_strata.restype = i32
         L.ipls_assign_ranges.argtypes = [vp, u32, u32, vp]; L.ipls_assign_ranges.restype = i32
+        L.ipls_assign_cuts.argtypes = [vp, u32, u32, vp, vp]; L.ipls_assign_cuts.restype = i32
         L.ipls_sort_segments.argtypes = [vp, sz, i32, ctypes.POINTER(_Config), vp, u32, u32, vp]
         L.ipls_sort_segments.restype = i32
         L.ipls_regroup_runs.argtypes = [vp, vp, vp, u32, u32, vp]; L.ipls_regroup_runs.restype = i32
@@ -331,6 +332,23 @@ def assign_ranges(counts, G: int) -> List[int]:
     b = np.zeros(G + 1, dtype=np.uint32)
     _check(lib().ipls_assign_ranges(c.ctypes.data, c.size, G, b.ctypes.data))
     return [int(x) for x in b]
+
+
+def assign_cuts(counts, G: int, splittable=None) -> List[int]:
+    """Global cut positions per rank; buckets flagged in `splittable` (one key value each)
+    may be split between ranks (host; ipls_assign_cuts)."""
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.uint64))
+    if c.size == 0:
+        raise ValueError("counts must not be empty")
+    sp = None
+    if splittable is not None:
+        sp = np.ascontiguousarray(np.asarray(splittable, dtype=np.uint8))
+        if sp.size != c.size:
+            raise ValueError("splittable must have one flag per bucket")
+    out = np.zeros(G + 1, dtype=np.uint64)
+    _check(lib().ipls_assign_cuts(c.ctypes.data, c.size, G,
+                                  None if sp is None else sp.ctypes.data, out.ctypes.data))
+    return [int(x) for x in out]
 
 
 @dataclass

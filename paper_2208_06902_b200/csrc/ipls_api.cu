@@ -1051,6 +1051,41 @@ ipls_status ipls_assign_ranges(const uint64_t* h_counts, uint32_t k, uint32_t G,
   return IPLS_OK;
 }
 
+ipls_status ipls_assign_cuts(const uint64_t* h_counts, uint32_t k, uint32_t G,
+                             const uint8_t* h_splittable, uint64_t* h_cuts) {
+  if (!h_counts || !h_cuts || k == 0 || G == 0) return IPLS_ERR_INVALID_ARGUMENT;
+  unsigned __int128 total = 0;
+  for (uint32_t b = 0; b < k; ++b) total += h_counts[b];
+  if (total > UINT64_MAX - 1) return IPLS_ERR_INVALID_ARGUMENT;
+  h_cuts[0] = 0;
+  uint32_t b = 0;                  // bucket whose start boundary `pre` is <= the last cut
+  unsigned __int128 pre = 0, prev = 0;
+  for (uint32_t r = 1; r < G; ++r) {
+    const unsigned __int128 target = total * r;
+    auto dist = [&](unsigned __int128 p) {
+      const unsigned __int128 x = p * G;
+      return x > target ? x - target : target - x;
+    };
+    unsigned __int128 best = prev, bestd = dist(prev), p = pre;
+    for (uint32_t c = b;; ++c) {   // boundary c at position p, then the inside of bucket c
+      if (p >= prev && dist(p) < bestd) { bestd = dist(p); best = p; }
+      if (p * G > target || c == k) break;  // past the target distances only grow
+      const unsigned __int128 e = p + h_counts[c];
+      if (h_splittable && h_splittable[c]) {
+        const unsigned __int128 q = target / G;  // floor and ceil of the ideal position
+        for (unsigned __int128 x = q; x <= q + 1; ++x)
+          if (x > p && x < e && x >= prev && dist(x) < bestd) { bestd = dist(x); best = x; }
+      }
+      p = e;
+    }
+    while (b < k && pre + h_counts[b] <= best) pre += h_counts[b++];
+    h_cuts[r] = (uint64_t)best;
+    prev = best;
+  }
+  h_cuts[G] = (uint64_t)total;
+  return IPLS_OK;
+}
+
 ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_key_type t,
                                  const ipls_model* h_model, uint64_t* d_offsets,
                                  uint16_t* d_bucket_ids, void* stream) {

@@ -12,9 +12,11 @@ sort.  A global array is the concatenation, in rank order, of every rank's shard
    Listing 1, P:410-463), so every rank holds the identical model (degenerate → EQ3, R5);
 3. partition — every rank partitions its shard by the model (`ipls_partition_level`,
    P:505-530, stable);
-4. plan — the per-rank bucket counts are all-gathered; `ipls_assign_ranges` gives rank r the
-   contiguous buckets [bounds[r], bounds[r+1]) balanced by count (buckets are range-ordered,
-   so contiguous bucket ranges are key ranges);
+4. plan — the per-rank bucket counts are all-gathered; `ipls_assign_cuts` gives rank r the
+   global positions [cuts[r], cuts[r+1]) of the bucket-major order balanced by count, cut
+   only at bucket boundaries (buckets are range-ordered, so contiguous bucket ranges are key
+   ranges) or inside EQ3's ==pivot bucket, which holds one key value (R5) and so can be
+   shared between ranks (a degenerate input still spreads evenly);
 5. exchange + finish — one all-to-all moves every bucket range to its rank; the rank puts
    the G runs it received (one per source, each bucket-major) into bucket-major order
    (`ipls_regroup_runs`) and resumes the recursion at level 1 with its buckets as the
@@ -40,7 +42,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from . import (DEFAULT_SEED, IPLSError, Model, assign_ranges, fit_fmcd, partition_level,
+from . import (DEFAULT_SEED, MODEL_EQ3, IPLSError, Model, assign_cuts, fit_fmcd, partition_level,
                regroup_runs, sample_size, sample_strata, sort, sort_segments, _key_type_of)
 
 
@@ -101,11 +103,35 @@ class CudaOps:
 @dataclass
 class DistResult:
     keys: object            # this rank's sorted key range (same dtype/device as the input)
-    bounds: List[int]       # bucket ranges: rank r holds buckets [bounds[r], bounds[r+1])
+    bounds: List[int]       # bounds[r]: first bucket boundary at or after cuts[r]
     model: Optional[Model]  # the shared top-level model (None when the global n < 8)
     counts: np.ndarray      # global bucket counts of the top level
     global_begin: int       # position of this rank's output in the sorted global array
     global_n: int
+    cuts: List[int]         # rank r holds global positions [cuts[r], cuts[r+1])
+
+
+def exchange_plan(cnt: np.ndarray, G: int, splittable=None):
+    """The exchange of step 4 from the G x k per-rank bucket counts (host).
+
+    cuts = ipls_assign_cuts of the global counts (positions in the bucket-major global order;
+    only `splittable` buckets may be cut inside); bounds[r] = the first bucket boundary at or
+    after cuts[r] (= ipls_assign_ranges' bounds when nothing is split); M[d][s, b] = how many
+    of source s's bucket-b keys land on rank d.  Source s's bucket-b keys occupy the global
+    positions pre[b] + sum(cnt[:s, b]) + [0, cnt[s, b]) (bucket-major, then rank order, then
+    the stable partition order), so each rank's share of a source's run is one contiguous
+    piece and the pieces for ranks 0..G-1 follow each other in the source's partitioned array.
+    """
+    cnt = np.asarray(cnt, dtype=np.int64)
+    total = cnt.sum(axis=0)
+    cuts = assign_cuts(total, G, splittable)
+    pre = np.concatenate([[0], np.cumsum(total)])
+    bounds = [int(np.searchsorted(pre, c, side="left")) for c in cuts[:G]] + [len(total)]
+    start = pre[:-1][None, :] + np.cumsum(cnt, axis=0) - cnt       # G x k first positions
+    end = start + cnt
+    M = [np.clip(np.minimum(end, cuts[d + 1]) - np.maximum(start, cuts[d]), 0, None)
+         for d in range(G)]
+    return cuts, bounds, M
 
 
 def _all_gather_int64(vals, group, device):
@@ -191,9 +217,11 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
     cnt = _all_gather_int64([off[b + 1] - off[b] for b in range(ke)], group, cdev)
     total = cnt.sum(axis=0)
     mark("partition")
-    bounds = assign_ranges(total, G)                              # step 4
-    send = [off[bounds[d + 1]] - off[bounds[d]] for d in range(G)]
-    recv = [int(cnt[s, bounds[r]:bounds[r + 1]].sum()) for s in range(G)]
+    # step 4: EQ3's ==pivot bucket holds one key value, so it may be split between ranks
+    split = [0, 1, 0] if model is not None and model.kind == MODEL_EQ3 and ke == 3 else None
+    cuts, bounds, M = exchange_plan(cnt, G, split)
+    send = [int(M[d][r].sum()) for d in range(G)]
+    recv = [int(M[r][s].sum()) for s in range(G)]
     out_w, status = attempt(lambda: torch.empty(sum(recv), dtype=torch.int64, device=cdev))
     if status == 0 and sum(recv) > 0xFFFFFFFF:
         status = 1  # IPLS_ERR_INVALID_ARGUMENT: beyond the ABI's 2^32 - 1 keys per call
@@ -204,7 +232,8 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
                            input_split_sizes=send, group=group)
     runs = out_w.to(dev).view(keys.dtype)
     mark("plan+exchange")
-    mine = cnt[:, bounds[r]:bounds[r + 1]]                        # G x (my buckets)
+    lo = bounds[r] - (1 if bounds[r] > 0 and total[:bounds[r]].sum() > cuts[r] else 0)
+    mine = M[r][:, lo:bounds[r + 1]]                              # G x (my buckets)
     out, status = attempt(lambda: ops.regroup(runs, mine))
     if status == 0:
         sizes = mine.sum(axis=0)
@@ -215,8 +244,7 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
     st = agree(status)
     if st:
         raise IPLSError(st, "in the distributed sort")
-    below = int(sum(cnt[:, :bounds[r]].sum(axis=1))) if bounds[r] > 0 else 0
-    return DistResult(out, bounds, model, total, below, gm)
+    return DistResult(out, bounds, model, total, cuts[r], gm, cuts)
 
 
 __all__ = ["dist_sort", "DistResult", "CudaOps"]

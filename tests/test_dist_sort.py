@@ -166,11 +166,17 @@ def test_dist_sort_matches_oracle_level0(world, kind):
         assert (model[0], model[1], model[2]) == (r0.A, r0.B, r0.D)
     else:
         assert model[3] == ipls.MODEL_EQ3 and model[4] == r0.pivot_ok
-    # rank r holds exactly the keys of buckets [bounds[r], bounds[r+1]) at its position
+    # rank r holds global positions [cuts[r], cuts[r+1]): bucket boundaries unless EQ3's
+    # ==pivot bucket is cut (bounds are then ipls_assign_ranges')
     pre = np.concatenate([[0], np.cumsum(counts)])
+    split = [0, 1, 0] if model[3] == ipls.MODEL_EQ3 else None
+    cuts = ipls.assign_cuts(counts, world, split)
+    if split is None:
+        assert bounds == ipls.assign_ranges(counts, world)
+        assert cuts == [int(pre[b]) for b in bounds]
     for r in res:
         rk = r[0]
-        assert r[6] == pre[bounds[rk]] and len(r[2]) == pre[bounds[rk + 1]] - pre[bounds[rk]]
+        assert r[6] == cuts[rk] and len(r[2]) == cuts[rk + 1] - cuts[rk]
         assert r[7] == n
 
 
@@ -201,6 +207,62 @@ def test_assign_ranges_is_argmin_per_boundary(G):
             cand = range(b[r - 1], k + 1)
             d = [abs(G * int(pre[x]) - r * tot) for x in cand]
             assert b[r] == b[r - 1] + int(np.argmin(d))  # argmin, ties to the lower boundary
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 5, 8])
+def test_assign_cuts_is_argmin_per_cut(G):
+    """ipls_assign_cuts against brute force over its candidates; without splittable buckets
+    it is ipls_assign_ranges in positions."""
+    rng = np.random.default_rng(100 + G)
+    for trial in range(200):
+        k = int(rng.integers(1, 12))
+        c = rng.integers(0, 9, k) * (rng.random(k) < 0.7)
+        if trial % 5 == 0:
+            c[:] = 0
+            c[rng.integers(0, k)] = int(rng.integers(1, 50))
+        pre = np.concatenate([[0], np.cumsum(c)])
+        tot = int(pre[-1])
+        cuts = ipls.assign_cuts(c, G)
+        assert cuts == [int(pre[b]) for b in ipls.assign_ranges(c, G)]
+        sp = rng.random(k) < 0.5
+        cuts = ipls.assign_cuts(c, G, sp)
+        cand = sorted(set(int(x) for x in pre) |
+                      {x for b in range(k) if sp[b] for x in range(pre[b] + 1, pre[b + 1])})
+        assert cuts[0] == 0 and cuts[G] == tot
+        for r in range(1, G):
+            ok = [x for x in cand if x >= cuts[r - 1]]
+            d = [abs(G * x - r * tot) for x in ok]
+            assert cuts[r] == ok[int(np.argmin(d))]  # argmin, ties to the lower candidate
+
+
+def test_exchange_plan_moves_every_key_once():
+    from paper_2208_06902_b200.distributed import exchange_plan
+    rng = np.random.default_rng(7)
+    for trial in range(100):
+        G, k = int(rng.integers(1, 6)), int(rng.integers(1, 10))
+        cnt = rng.integers(0, 7, (G, k)) * (rng.random((G, k)) < 0.8)
+        sp = rng.random(k) < 0.4
+        cuts, bounds, M = exchange_plan(cnt, G, sp)
+        assert np.array_equal(sum(M), cnt)                    # every key goes to one rank
+        for d in range(G):
+            assert int(M[d].sum()) == cuts[d + 1] - cuts[d]
+            pre = np.concatenate([[0], np.cumsum(cnt.sum(axis=0))])
+            assert pre[bounds[d]] >= cuts[d] and (bounds[d] == 0 or pre[bounds[d] - 1] < cuts[d]
+                                                  or cnt.sum(axis=0)[bounds[d] - 1] == 0)
+            for b in range(k):                                # only splittable buckets shared
+                if not sp[b] and 0 < M[d][:, b].sum() < cnt[:, b].sum():
+                    raise AssertionError((trial, d, b))
+        if not sp.any():
+            assert bounds == ipls.assign_ranges(cnt.sum(axis=0), G)
+
+
+def test_dist_sort_splits_a_degenerate_input_evenly():
+    """All keys equal: EQ3 puts them in the ==pivot bucket, which is cut between the ranks."""
+    world, n = 3, 30000
+    res = _run(world, "all_equal", n)
+    assert all(r[1] == "ok" for r in res)
+    assert [len(r[2]) for r in res] == [10000, 10000, 10000]
+    assert [r[6] for r in res] == [0, 10000, 20000]
 
 
 def test_sample_size_matches_oracle():
