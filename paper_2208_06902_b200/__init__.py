@@ -16,7 +16,7 @@ from typing import List, Optional
 import numpy as np
 
 __all__ = [
-    "IPLSError", "lib", "sort", "sort_host", "fit_fmcd", "partition_level", "sort_trace",
+    "IPLSError", "lib", "sort", "sort_host", "sort_host_batch", "fit_fmcd", "partition_level", "sort_trace",
     "workspace_bytes", "Model", "Record", "KEY_F64", "KEY_U64", "MODEL_LINEAR", "MODEL_EQ3", "MODEL_TREE",
     "DEFAULT_SEED", "launch_count", "sample_size", "sample_strata", "assign_ranges", "assign_cuts",
 ]
@@ -80,7 +80,7 @@ class _ProfEntry(ctypes.Structure):
 
 # C-ABI symbols declared in include/ipls.h (tests check the .so exports all of them)
 SYMBOLS = ["ipls_default_config", "ipls_sort_f64", "ipls_sort_u64", "ipls_sort_ex",
-           "ipls_workspace_bytes", "ipls_sort_host", "ipls_fit_fmcd", "ipls_partition_level",
+           "ipls_workspace_bytes", "ipls_sort_host", "ipls_sort_host_batch", "ipls_fit_fmcd", "ipls_partition_level",
            "ipls_sort_trace", "ipls_status_string", "ipls_last_cuda_error",
            "ipls_kernel_launch_count", "ipls_profile_enable", "ipls_profile_reset",
            "ipls_profile_read", "ipls_sample_size", "ipls_sample_strata", "ipls_assign_ranges", "ipls_assign_cuts", "ipls_fit_sample", "ipls_debug_set_epoch",
@@ -108,6 +108,8 @@ def lib():
         L.ipls_workspace_bytes.restype = sz
         L.ipls_sort_host.argtypes = [vp, sz, i32, ctypes.POINTER(_Config), vp]
         L.ipls_sort_host.restype = i32
+        L.ipls_sort_host_batch.argtypes = [vp, vp, vp, u32, i32, ctypes.POINTER(_Config), vp]
+        L.ipls_sort_host_batch.restype = i32
         L.ipls_fit_fmcd.argtypes = [vp, sz, i32, u32, ctypes.POINTER(_Model), vp]
         L.ipls_fit_fmcd.restype = i32
         L.ipls_partition_level.argtypes = [vp, vp, sz, i32, ctypes.POINTER(_Model), vp, vp, vp]
@@ -259,6 +261,20 @@ def sort_host_ptr(ptr: int, n: int, key_type: int, k: int = 256, base_case: int 
                   seed: int = DEFAULT_SEED, stream=None, model: int = MODEL_LINEAR) -> None:
     c = _cfg(k, base_case, seed, model)
     _check(lib().ipls_sort_host(ptr, n, key_type, ctypes.byref(c), _stream(stream)))
+
+
+def sort_host_batch(ins, outs, sizes, key_type: int, k: int = 256, base_case: int = 4096,
+                    seed: int = DEFAULT_SEED, stream=None, model: int = MODEL_LINEAR) -> None:
+    """Sort `len(ins)` host arrays given as raw pointers (ins[j] -> outs[j], sizes[j] keys),
+    with the copies pipelined against the sorts (ipls_sort_host_batch)."""
+    m = len(ins)
+    if len(outs) != m or len(sizes) != m:
+        raise ValueError("ins, outs and sizes must have the same length")
+    pi = (ctypes.c_void_p * max(m, 1))(*ins)
+    po = (ctypes.c_void_p * max(m, 1))(*outs)
+    pn = (ctypes.c_size_t * max(m, 1))(*sizes)
+    c = _cfg(k, base_case, seed, model)
+    _check(lib().ipls_sort_host_batch(pi, po, pn, m, key_type, ctypes.byref(c), _stream(stream)))
 
 
 @dataclass

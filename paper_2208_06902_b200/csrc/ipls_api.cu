@@ -939,6 +939,77 @@ ipls_status ipls_sort_host(void* h_keys, size_t n, ipls_key_type t, const ipls_c
   }
 }
 
+// Two internal streams per device for ipls_sort_host_batch (created once, kept).
+struct PipeStreams {
+  cudaStream_t s[2];
+  cudaEvent_t ev;
+};
+PipeStreams& pipe_streams() {
+  static std::map<int, PipeStreams> m;
+  int dev = 0;
+  ck(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = m.find(dev);
+  if (it == m.end()) {
+    PipeStreams p;
+    ck(cudaStreamCreateWithFlags(&p.s[0], cudaStreamNonBlocking));
+    ck(cudaStreamCreateWithFlags(&p.s[1], cudaStreamNonBlocking));
+    ck(cudaEventCreateWithFlags(&p.ev, cudaEventDisableTiming));
+    it = m.emplace(dev, p).first;
+  }
+  return it->second;
+}
+
+ipls_status ipls_sort_host_batch(const void* const* h_in, void* const* h_out, const size_t* n,
+                                 uint32_t count, ipls_key_type t, const ipls_config* cfg,
+                                 void* stream) {
+  if (count == 0) return IPLS_OK;
+  if (!h_in || !h_out || !n) return IPLS_ERR_INVALID_ARGUMENT;
+  for (uint32_t j = 0; j < count; ++j)
+    if (n[j] > 0 && (!h_in[j] || !h_out[j])) return IPLS_ERR_INVALID_ARGUMENT;
+  if (t != IPLS_KEY_F64 && t != IPLS_KEY_U64) return IPLS_ERR_INVALID_ARGUMENT;
+  {
+    ipls_config c;
+    const ipls_status s = check_cfg(cfg, &c);
+    if (s != IPLS_OK) return s;
+  }
+  try {
+    PipeStreams& ps = pipe_streams();
+    // the batch starts after the work already queued on the caller's stream
+    ck(cudaEventRecord(ps.ev, static_cast<cudaStream_t>(stream)));
+    ck(cudaStreamWaitEvent(ps.s[0], ps.ev, 0));
+    ck(cudaStreamWaitEvent(ps.s[1], ps.ev, 0));
+    auto upload = [&](uint32_t j) {  // array j into its stream's device buffer
+      if (n[j] <= 1) return;
+      cudaStream_t s = ps.s[j & 1];
+      StreamCache& sc = cache_for(s);
+      sc.io.ensure(n[j] * 8);  // stream-ordered after this buffer's previous download
+      ck(cudaMemcpyAsync(sc.io.ptr, h_in[j], n[j] * 8, cudaMemcpyHostToDevice, s));
+    };
+    ipls_status st = IPLS_OK;
+    upload(0);
+    for (uint32_t j = 0; j < count && st == IPLS_OK; ++j) {
+      if (j + 1 < count) upload(j + 1);  // overlaps this sort and the previous download
+      if (n[j] == 0) continue;
+      if (n[j] == 1) {
+        std::memmove(h_out[j], h_in[j], 8);
+        continue;
+      }
+      cudaStream_t s = ps.s[j & 1];
+      StreamCache& sc = cache_for(s);
+      st = sort_impl(sc.io.ptr, n[j], t, cfg, nullptr, 0, s, nullptr);
+      if (st == IPLS_OK)
+        ck(cudaMemcpyAsync(h_out[j], sc.io.ptr, n[j] * 8, cudaMemcpyDeviceToHost, s));
+    }
+    ck(cudaStreamSynchronize(ps.s[0]));
+    ck(cudaStreamSynchronize(ps.s[1]));
+    return st;
+  } catch (const CudaFail& f) {
+    g_last_cuda_error = cudaGetErrorString(f.e);
+    return f.e == cudaErrorMemoryAllocation ? IPLS_ERR_OUT_OF_MEMORY : IPLS_ERR_CUDA;
+  }
+}
+
 static ipls_status fit_given(const void* d_sorted_sample, size_t S, ipls_key_type t, uint32_t k,
                              ipls_model* h_out, void* stream, int sort_given);
 

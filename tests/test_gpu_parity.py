@@ -464,6 +464,38 @@ def test_sort_host_e2e(ipls):
     assert h.numpy().tobytes() == want.tobytes()
 
 
+def test_sort_host_batch(ipls):
+    """ipls_sort_host_batch: pipelined host arrays of mixed sizes (empty, one key, sizes
+    that reallocate the internal buffers, u64 above 2^53), some in place; outputs bit-exact."""
+    rng = np.random.default_rng(11)
+    arrs = [datagen.generate("C2", 2_000_000), np.zeros(0), np.array([2.5]),
+            datagen.generate("C3", 3_000_001), rng.normal(size=100_000),
+            np.repeat(rng.normal(size=1000), 1000)]
+    ins = [torch.from_numpy(x.copy()).pin_memory() for x in arrs]
+    outs = [torch.empty(x.size, dtype=torch.float64).pin_memory() for x in arrs]
+    outs[2] = ins[2]  # in place
+    outs[4] = ins[4]
+    ipls.sort_host_batch([t.data_ptr() for t in ins], [t.data_ptr() for t in outs],
+                         [x.size for x in arrs], ipls.KEY_F64, k=1024, base_case=4096)
+    for x, o in zip(arrs, outs):
+        assert o.numpy().tobytes() == np.sort(x).tobytes()
+    u = rng.integers(0, 2**64 - 1, 500_000, dtype=np.uint64, endpoint=True)
+    hu = [torch.from_numpy(u.view(np.int64).copy()).pin_memory() for _ in range(3)]
+    ipls.sort_host_batch([t.data_ptr() for t in hu], [t.data_ptr() for t in hu], [u.size] * 3,
+                         ipls.KEY_U64, k=1024, base_case=4096)
+    for t in hu:
+        assert t.numpy().view(np.uint64).tobytes() == np.sort(u).tobytes()
+    bad = datagen.generate("C2", 100_000)
+    bad[777] = np.nan
+    hb = torch.from_numpy(bad).pin_memory()
+    with pytest.raises(ipls.IPLSError) as e:
+        ipls.sort_host_batch([hb.data_ptr()], [hb.data_ptr()], [bad.size], ipls.KEY_F64,
+                             k=1024, base_case=4096)
+    assert e.value.status == 2
+    with pytest.raises(ipls.IPLSError):
+        ipls.sort_host_batch([0], [0], [5], ipls.KEY_F64)
+
+
 def test_caller_workspace(ipls):
     a = datagen.generate("C3", 1_000_000)
     want = np.sort(a)
