@@ -101,13 +101,13 @@ ipls_status ipls_sort_host(void* h_keys, size_t n, ipls_key_type t, const ipls_c
 
 /* Sort `count` HOST arrays (P:637's sorting rate for data that starts and ends in host
  * memory): array j is copied from h_in[j] to the device, sorted as ipls_sort_ex sorts it, and
- * copied back to h_out[j] (which may equal h_in[j]).  The copies are pipelined over two
- * internal streams: array j+1's host-to-device copy is issued before array j is sorted, so it
- * overlaps that sort and array j-1's device-to-host copy (the PCIe link carries both
- * directions at once).  The batch starts after the work queued on `stream`; the call returns
+ * copied back to h_out[j] (which may equal h_in[j]).  The copies are pipelined over three
+ * internal streams, each with its own device buffer: array j+1's host-to-device copy is issued
+ * before array j is sorted, so it overlaps that sort and the earlier arrays' device-to-host
+ * copies (the PCIe link carries both directions at once).  The batch starts after the work queued on `stream`; the call returns
  * when every output is written.  h_in[j], h_out[j]: host (pinned for overlap), n[j] keys each;
- * distinct outputs must not overlap each other or another array's input.  Device memory: two
- * io buffers and two workspaces (one per internal stream), cached.  Errors: INVALID_ARGUMENT
+ * distinct outputs must not overlap each other or another array's input.  Device memory:
+ * three io buffers and three workspaces (one per internal stream), cached.  Errors: INVALID_ARGUMENT
  * (NULL arrays, a NULL buffer with n[j] > 0, bad key type or config), the first sort's error
  * (e.g. NAN_KEY: arrays from that one on are left unspecified), OUT_OF_MEMORY, CUDA. */
 ipls_status ipls_sort_host_batch(const void* const* h_in, void* const* h_out, const size_t* n,

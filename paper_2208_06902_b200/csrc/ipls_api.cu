@@ -939,9 +939,12 @@ ipls_status ipls_sort_host(void* h_keys, size_t n, ipls_key_type t, const ipls_c
   }
 }
 
-// Two internal streams per device for ipls_sort_host_batch (created once, kept).
+// Internal streams per device for ipls_sort_host_batch (created once, kept).  Array j uses
+// stream j % kPipe and its device buffer: with three, array j+1's upload waits only for array
+// j-2's download, so the uploads run back to back.
+constexpr int kPipe = 3;
 struct PipeStreams {
-  cudaStream_t s[2];
+  cudaStream_t s[kPipe];
   cudaEvent_t ev;
 };
 PipeStreams& pipe_streams() {
@@ -952,8 +955,7 @@ PipeStreams& pipe_streams() {
   auto it = m.find(dev);
   if (it == m.end()) {
     PipeStreams p;
-    ck(cudaStreamCreateWithFlags(&p.s[0], cudaStreamNonBlocking));
-    ck(cudaStreamCreateWithFlags(&p.s[1], cudaStreamNonBlocking));
+    for (int i = 0; i < kPipe; ++i) ck(cudaStreamCreateWithFlags(&p.s[i], cudaStreamNonBlocking));
     ck(cudaEventCreateWithFlags(&p.ev, cudaEventDisableTiming));
     it = m.emplace(dev, p).first;
   }
@@ -977,11 +979,10 @@ ipls_status ipls_sort_host_batch(const void* const* h_in, void* const* h_out, co
     PipeStreams& ps = pipe_streams();
     // the batch starts after the work already queued on the caller's stream
     ck(cudaEventRecord(ps.ev, static_cast<cudaStream_t>(stream)));
-    ck(cudaStreamWaitEvent(ps.s[0], ps.ev, 0));
-    ck(cudaStreamWaitEvent(ps.s[1], ps.ev, 0));
+    for (int i = 0; i < kPipe; ++i) ck(cudaStreamWaitEvent(ps.s[i], ps.ev, 0));
     auto upload = [&](uint32_t j) {  // array j into its stream's device buffer
       if (n[j] <= 1) return;
-      cudaStream_t s = ps.s[j & 1];
+      cudaStream_t s = ps.s[j % kPipe];
       StreamCache& sc = cache_for(s);
       sc.io.ensure(n[j] * 8);  // stream-ordered after this buffer's previous download
       ck(cudaMemcpyAsync(sc.io.ptr, h_in[j], n[j] * 8, cudaMemcpyHostToDevice, s));
@@ -995,14 +996,13 @@ ipls_status ipls_sort_host_batch(const void* const* h_in, void* const* h_out, co
         std::memmove(h_out[j], h_in[j], 8);
         continue;
       }
-      cudaStream_t s = ps.s[j & 1];
+      cudaStream_t s = ps.s[j % kPipe];
       StreamCache& sc = cache_for(s);
       st = sort_impl(sc.io.ptr, n[j], t, cfg, nullptr, 0, s, nullptr);
       if (st == IPLS_OK)
         ck(cudaMemcpyAsync(h_out[j], sc.io.ptr, n[j] * 8, cudaMemcpyDeviceToHost, s));
     }
-    ck(cudaStreamSynchronize(ps.s[0]));
-    ck(cudaStreamSynchronize(ps.s[1]));
+    for (int i = 0; i < kPipe; ++i) ck(cudaStreamSynchronize(ps.s[i]));
     return st;
   } catch (const CudaFail& f) {
     g_last_cuda_error = cudaGetErrorString(f.e);
