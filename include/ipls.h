@@ -154,16 +154,19 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
  * at `level`: each segment of more than base_case keys is partitioned as a
  * level-`level` segment (its sample drawn with that level's hash, R2/R18, as if an earlier
  * level had produced it), each smaller one goes to the base case.  This is the local
- * sort of the multi-GPU top level: with level = 1 and the top level's buckets,
- * in global order, as the segments, every model and layout below the top level equals the
- * one-GPU sort's.  d_keys: device, n keys sorted in place.  h_seg_sizes: host, nseg sizes
- * summing to n (zeros allowed).  Uses the stream's internal workspace.  Errors: as
+ * sort of the multi-GPU top level: with level = 1, the top level's buckets, in
+ * global order, as the segments and global_begin = the position of d_keys[0] in the global
+ * bucket-major order, every model and layout below the top level equals the one-GPU sort's.
+ * global_begin only enters the sampling hash (R18 hashes a segment's begin; here begin =
+ * global_begin + the segment's offset in d_keys); addressing stays local.  d_keys: device, n
+ * keys sorted in place.  h_seg_sizes: host, nseg sizes summing to n (zeros allowed).  Uses
+ * the stream's internal workspace.  Errors: as
  * ipls_sort_ex (NaN: the array is left unmodified), INVALID_ARGUMENT if the sizes do not sum
  * to n.  The segments are trusted to be range-ordered (not checked); if they are not, the
  * output is not sorted. */
 ipls_status ipls_sort_segments(void* d_keys, size_t n, ipls_key_type t, const ipls_config* cfg,
                                const uint64_t* h_seg_sizes, uint32_t nseg, uint32_t level,
-                               void* stream);
+                               uint64_t global_begin, void* stream);
 
 /* Multi-GPU exchange: the receiving rank holds G runs back to back, run g
  * (from source rank g, in rank order) holding that source's keys of buckets b0 .. b0+nb-1,
@@ -239,8 +242,8 @@ ipls_status ipls_sort_trace(void* d_keys, size_t n, ipls_key_type t, const ipls_
  * level, starting at `level`; snapshots by iteration).  Same arguments and errors. */
 ipls_status ipls_sort_segments_trace(void* d_keys, size_t n, ipls_key_type t,
                                      const ipls_config* cfg, const uint64_t* h_seg_sizes,
-                                     uint32_t nseg, uint32_t level, ipls_trace* trace,
-                                     void* stream);
+                                     uint32_t nseg, uint32_t level, uint64_t global_begin,
+                                     ipls_trace* trace, void* stream);
 
 const char* ipls_status_string(ipls_status s);
 const char* ipls_last_cuda_error(void);

@@ -133,11 +133,12 @@ def lib():
         L.ipls_sample_strata.restype = i32
         L.ipls_assign_ranges.argtypes = [vp, u32, u32, vp]; L.ipls_assign_ranges.restype = i32
         L.ipls_assign_cuts.argtypes = [vp, u32, u32, vp, vp]; L.ipls_assign_cuts.restype = i32
-        L.ipls_sort_segments.argtypes = [vp, sz, i32, ctypes.POINTER(_Config), vp, u32, u32, vp]
+        L.ipls_sort_segments.argtypes = [vp, sz, i32, ctypes.POINTER(_Config), vp, u32, u32,
+                                         ctypes.c_uint64, vp]
         L.ipls_sort_segments.restype = i32
         L.ipls_regroup_runs.argtypes = [vp, vp, vp, u32, u32, vp]; L.ipls_regroup_runs.restype = i32
         L.ipls_sort_segments_trace.argtypes = [vp, sz, i32, ctypes.POINTER(_Config), vp, u32, u32,
-                                               ctypes.POINTER(_Trace), vp]
+                                               ctypes.c_uint64, ctypes.POINTER(_Trace), vp]
         L.ipls_sort_segments_trace.restype = i32
         _lib = L
     return _lib
@@ -218,16 +219,17 @@ def sort(keys, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SEED,
 
 def sort_segments(keys, sizes, level: int = 1, k: int = 256, base_case: int = 4096,
                   seed: int = DEFAULT_SEED, key_type: Optional[int] = None, stream=None,
-                  model: int = MODEL_LINEAR) -> None:
+                  model: int = MODEL_LINEAR, global_begin: int = 0) -> None:
     """Sort in place a CUDA tensor made of consecutive range-ordered segments of the given
-    sizes, resuming the recursion at `level` (ipls_sort_segments)."""
+    sizes, resuming the recursion at `level` (ipls_sort_segments); global_begin: the
+    position of keys[0] in the array whose recursion is resumed (sampling hash only)."""
     _check_tensor(keys)
     kt = _key_type_of(keys, key_type)
     c = _cfg(k, base_case, seed, model)
     sz = np.ascontiguousarray(np.asarray(sizes, dtype=np.uint64))
     _check(lib().ipls_sort_segments(keys.data_ptr(), keys.numel(), kt, ctypes.byref(c),
                                     sz.ctypes.data if sz.size else None, int(sz.size),
-                                    int(level), _stream(stream)))
+                                    int(level), int(global_begin), _stream(stream)))
 
 
 def regroup_runs(src, dst, counts, stream=None) -> None:
@@ -396,7 +398,7 @@ def sort_trace(keys, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SE
                key_type: Optional[int] = None, snapshot_levels: int = 0, stream=None,
                max_records: int = 1 << 16, max_counts: int = 1 << 24,
                max_samples: int = 1 << 24, model: int = MODEL_LINEAR, segments=None,
-               level: int = 1) -> TraceResult:
+               level: int = 1, global_begin: int = 0) -> TraceResult:
     """Sort in place and return the per-segment trace (records ordered by level, begin).
     segments: sizes of range-ordered segments to resume from at `level`
     (ipls_sort_segments_trace) instead of a whole sort."""
@@ -424,7 +426,8 @@ def sort_trace(keys, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SE
             sz = np.ascontiguousarray(np.asarray(segments, dtype=np.uint64))
             _check(lib().ipls_sort_segments_trace(keys.data_ptr(), n, kt, ctypes.byref(c),
                                                   sz.ctypes.data if sz.size else None,
-                                                  int(sz.size), int(level), ctypes.byref(tr),
+                                                  int(sz.size), int(level), int(global_begin),
+                                                  ctypes.byref(tr),
                                                   _stream(stream)))
         if tr.records_len <= max_records and tr.counts_len <= max_counts and \
                 tr.samples_len <= max_samples:

@@ -392,6 +392,7 @@ struct InitSegs {
   const uint64_t* sizes;  // host, nseg entries summing to n
   uint32_t nseg;
   uint32_t level;
+  uint64_t hash_base;     // position of the array in the one whose recursion is resumed
 };
 
 // Greedy left-to-right packing of the base-case segments of an initial segment list into
@@ -442,6 +443,7 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
   const uint32_t k = p.k;
 
   const uint32_t level0 = init ? init->level : 0u;
+  const uint64_t hbase = init ? init->hash_base : 0u;  // sampling hash: segment begin + hbase
   if (!init && n <= p.B) {
     // The root is a base-case segment: one window in place.
     Window w{0, (uint32_t)n, 0};
@@ -595,16 +597,16 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
       uint32_t* redo_cnt = &cctr->n_redo;                 // zero: cleared with the counters
       if (max_S <= (uint32_t)kFMMax)
         k_fit_small<F64, kFSThreads, kFMItems><<<nseg, kFSThreads, kFMSmem, st>>>(
-            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
+            src, segs, seed, hbase, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
       else if (max_S <= (uint32_t)kFSMax)
         k_fit_small<F64, kFSThreads, kFSItems><<<nseg, kFSThreads, kFSSmem, st>>>(
-            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
+            src, segs, seed, hbase, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
       else
         k_fit_small<F64, kFLThreads, kFLItems><<<nseg, kFLThreads, kFLSmem, st>>>(
-            src, segs, seed, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
+            src, segs, seed, hbase, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
       ck_launch();
       k_gather_fit<F64><<<std::min(nseg, num_sms()), kFitThreads, fit_smem(cap), st>>>(
-          src, segs, seed, level, k, cap, trace ? samples : nullptr, models, nullptr, redo, tree, 0,
+          src, segs, seed, hbase, level, k, cap, trace ? samples : nullptr, models, nullptr, redo, tree, 0,
           redo_cnt);
       ck_launch();
     }
@@ -843,29 +845,31 @@ ipls_status ipls_sort_trace(void* d_keys, size_t n, ipls_key_type t, const ipls_
 
 static ipls_status sort_segments_impl(void* d_keys, size_t n, ipls_key_type t,
                                       const ipls_config* cfg, const uint64_t* h_seg_sizes,
-                                      uint32_t nseg, uint32_t level, ipls_trace* tr,
-                                      void* stream) {
+                                      uint32_t nseg, uint32_t level, uint64_t global_begin,
+                                      ipls_trace* tr, void* stream) {
   if (nseg == 0 || !h_seg_sizes) return n == 0 ? IPLS_OK : IPLS_ERR_INVALID_ARGUMENT;
   unsigned __int128 tot = 0;
   for (uint32_t i = 0; i < nseg; ++i) tot += h_seg_sizes[i];
   if (tot != n) return IPLS_ERR_INVALID_ARGUMENT;
   if (n <= 1) return sort_impl(d_keys, n, t, cfg, nullptr, 0, stream, tr);
-  const InitSegs init{h_seg_sizes, nseg, level};
+  const InitSegs init{h_seg_sizes, nseg, level, global_begin};
   return sort_impl(d_keys, n, t, cfg, nullptr, 0, stream, tr, &init);
 }
 
 ipls_status ipls_sort_segments(void* d_keys, size_t n, ipls_key_type t, const ipls_config* cfg,
                                const uint64_t* h_seg_sizes, uint32_t nseg, uint32_t level,
-                               void* stream) {
-  return sort_segments_impl(d_keys, n, t, cfg, h_seg_sizes, nseg, level, nullptr, stream);
+                               uint64_t global_begin, void* stream) {
+  return sort_segments_impl(d_keys, n, t, cfg, h_seg_sizes, nseg, level, global_begin, nullptr,
+                            stream);
 }
 
 ipls_status ipls_sort_segments_trace(void* d_keys, size_t n, ipls_key_type t,
                                      const ipls_config* cfg, const uint64_t* h_seg_sizes,
-                                     uint32_t nseg, uint32_t level, ipls_trace* trace,
-                                     void* stream) {
+                                     uint32_t nseg, uint32_t level, uint64_t global_begin,
+                                     ipls_trace* trace, void* stream) {
   if (!trace) return IPLS_ERR_INVALID_ARGUMENT;
-  return sort_segments_impl(d_keys, n, t, cfg, h_seg_sizes, nseg, level, trace, stream);
+  return sort_segments_impl(d_keys, n, t, cfg, h_seg_sizes, nseg, level, global_begin, trace,
+                            stream);
 }
 
 ipls_status ipls_regroup_runs(const void* d_src, void* d_dst, const uint64_t* h_counts,
@@ -1046,12 +1050,12 @@ static ipls_status fit_given(const void* d_sorted_sample, size_t S, ipls_key_typ
     const uint32_t cap = fit_cap((uint32_t)S);
     if (t == IPLS_KEY_F64) {
       set_attrs<true>();
-      k_gather_fit<true><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, k, cap,
+      k_gather_fit<true><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, 0, k, cap,
                                                                 nullptr, dmod, smp, nullptr,
                                                                 nullptr, sort_given);
     } else {
       set_attrs<false>();
-      k_gather_fit<false><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, k, cap,
+      k_gather_fit<false><<<1, kFitThreads, fit_smem(cap), st>>>(nullptr, dseg, 0, 0, 0, k, cap,
                                                                  nullptr, dmod, smp, nullptr,
                                                                  nullptr, sort_given);
     }

@@ -248,7 +248,7 @@ __device__ __forceinline__ void write_tree(const uint64_t* so, uint32_t S, uint3
 template <bool F64>
 __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
-    uint32_t level, uint32_t k, uint32_t cap, uint64_t* __restrict__ samples_out,
+    uint64_t hbase, uint32_t level, uint32_t k, uint32_t cap, uint64_t* __restrict__ samples_out,
     ModelDev* __restrict__ models, const uint64_t* __restrict__ presorted_ok,
     const uint32_t* __restrict__ redo, uint64_t* __restrict__ tree, int sort_given = 0,
     const uint32_t* __restrict__ redo_cnt = nullptr) {
@@ -274,7 +274,8 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     __syncthreads();
     if (sort_given) block_sort_ok<kFitThreads>(a, tmp, fh, S, ss);  // ipls_fit_sample
   } else {
-    const uint64_t t = sm64(sm64(sm64(seed) ^ (uint64_t)level) ^ sg.begin);
+    // hbase: position of this array in the one whose recursion is resumed (ipls_sort_segments)
+    const uint64_t t = sm64(sm64(sm64(seed) ^ (uint64_t)level) ^ (sg.begin + hbase));
     StrataWalk sw(threadIdx.x, kFitThreads, sg.m, S);
     // batches of 8 loads in flight per thread (S <= cap <= 8 kFitThreads)
     for (uint32_t j0 = threadIdx.x; j0 < S; j0 += 8 * kFitThreads) {
@@ -385,7 +386,8 @@ constexpr size_t kFLSmem = (size_t)kFLMax * 12;
 template <bool F64, int NT, int IT>
 __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
     const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
-    uint32_t level, uint32_t k, uint64_t* __restrict__ samples_out, ModelDev* __restrict__ models,
+    uint64_t hbase, uint32_t level, uint32_t k, uint64_t* __restrict__ samples_out,
+    ModelDev* __restrict__ models,
     uint32_t* __restrict__ redo, uint64_t* __restrict__ tree, uint32_t* __restrict__ redo_cnt) {
   constexpr int NW = NT / 32, SMAX = NT * IT;
   static_assert(NT >= 256 && IT % 4 == 0, "256 coarse bins, uint4 fine-bin scan");
@@ -408,7 +410,8 @@ __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
 #else
 #define FITL_TICK(N)
 #endif
-  const uint64_t t = sm64(sm64(sm64(seed) ^ (uint64_t)level) ^ sg.begin);
+  // hbase: position of this array in the one whose recursion is resumed (ipls_sort_segments)
+    const uint64_t t = sm64(sm64(sm64(seed) ^ (uint64_t)level) ^ (sg.begin + hbase));
   StrataWalk sw(threadIdx.x, NT, sg.m, S);
   uint64_t v[IT];
   uint64_t mn = ~0ull, mx = 0ull;

@@ -89,12 +89,13 @@ class CudaOps:
         return out
 
     def sort_segments(self, keys, key_type: int, k: int, base_case: int, seed: int, sizes,
-                      level: int) -> int:
-        """Sort range-ordered segments from `level` on (ipls_sort_segments); returns the
-        status instead of raising (see sort)."""
+                      level: int, global_begin: int = 0) -> int:
+        """Sort range-ordered segments from `level` on (ipls_sort_segments; global_begin =
+        the position of keys[0] in the global order); returns the status instead of raising
+        (see sort)."""
         try:
             sort_segments(keys, sizes, level=level, k=k, base_case=base_case, seed=seed,
-                          key_type=key_type, stream=self.stream)
+                          key_type=key_type, stream=self.stream, global_begin=global_begin)
             return 0
         except IPLSError as e:
             return e.status
@@ -237,7 +238,7 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
     out, status = attempt(lambda: ops.regroup(runs, mine))
     if status == 0:
         sizes = mine.sum(axis=0)
-        status = ops.sort_segments(out, kt, k, base_case, seed, sizes, 1)
+        status = ops.sort_segments(out, kt, k, base_case, seed, sizes, 1, cuts[r])
     else:
         out = runs
     mark("local sort")

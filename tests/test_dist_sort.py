@@ -89,7 +89,7 @@ class OracleOps:
         out = np.concatenate(flat) if flat else bits[:0]
         return torch.from_numpy(out.copy()).view(runs.dtype)
 
-    def sort_segments(self, t, kt, k, base_case, seed, sizes, level):
+    def sort_segments(self, t, kt, k, base_case, seed, sizes, level, global_begin=0):
         # the segments are range-ordered: sorting the whole range sorts each of them
         assert int(np.sum(sizes)) == t.numel()
         return self.sort(t, kt, k, base_case, seed)

@@ -235,11 +235,14 @@ def test_sort_segments_nan_leaves_array_unmodified(ipls):
 def test_simulated_ranks_data_path(ipls, G):
     """The N-rank data path of dist_sort on one GPU (no rank waits on another): the global
     level-0 model, every shard's stable partition, the exchange as slicing, regroup and the
-    resumed local sorts; the concatenation is the sorted input."""
+    resumed local sorts with the rank's global position as hash base; the concatenation is the
+    sorted input, and every record below level 0 on every rank is the one-GPU sort's record of
+    the same (level, global begin)."""
     a = datagen.generate("C5", 2_000_000)
     n = a.size
     cfg = datagen.CONFIGS["C5"]
-    r0 = oracle.sort(a.copy(), k=cfg.k, base_case=cfg.base_case, trace=True).records[0]
+    ores = oracle.sort(a.copy(), k=cfg.k, base_case=cfg.base_case, trace=True)
+    r0 = ores.records[0]
     mdl = ipls.Model(r0.A, r0.B, r0.k_eff, r0.D, r0.kind, r0.capped, r0.pivot_ok)
     shards = np.array_split(a, G)
     parts, offs = [], []
@@ -250,7 +253,9 @@ def test_simulated_ranks_data_path(ipls, G):
         offs.append(off.cpu().numpy().astype(np.int64))
     cnt = np.stack([np.diff(o) for o in offs])
     bounds = ipls.assign_ranges(cnt.sum(axis=0), G)
-    out = []
+    pre = np.concatenate([[0], np.cumsum(cnt.sum(axis=0))])
+    want = {(o.level, o.begin): o for o in ores.records if o.level >= 1}
+    out, seen = [], 0
     for r in range(G):
         b0, b1 = bounds[r], bounds[r + 1]
         runs = torch.cat([parts[s][int(offs[s][b0]):int(offs[s][b1])] for s in range(G)])
@@ -258,8 +263,20 @@ def test_simulated_ranks_data_path(ipls, G):
         reg = torch.empty_like(runs)
         if runs.numel():
             ipls.regroup_runs(runs, reg, mine)
-            ipls.sort_segments(reg, mine.sum(axis=0), level=1, k=cfg.k, base_case=cfg.base_case,
-                               key_type=0)
+            tr = ipls.sort_trace(reg, k=cfg.k, base_case=cfg.base_case, key_type=0,
+                                 segments=mine.sum(axis=0), level=1, global_begin=int(pre[b0]))
+            for g in tr.records:
+                o = want.get((g.level, g.begin + int(pre[b0])))
+                if o is None:  # only one-valued segments may be extra (see above)
+                    assert g.kind == ipls.MODEL_EQ3 and g.counts[1] == g.m
+                    continue
+                seen += 1
+                assert (g.m, g.S, g.kind, g.D, g.capped, g.pivot_ok) == \
+                    (o.m, o.S, o.kind, o.D, o.capped, o.pivot_ok)
+                assert g.A == o.A and g.B == o.B
+                assert np.array_equal(g.counts, o.counts)
+                assert np.array_equal(g.sample, o.sample)
         out.append(reg.cpu().numpy())
     got = np.concatenate(out).view(np.float64)
     assert got.tobytes() == _ok_sorted(a).tobytes()
+    assert seen == len(want)  # every one-GPU record below level 0 was reproduced
