@@ -255,10 +255,13 @@ void ipls_debug_set_epoch(uint32_t e);
  * same-address lanes of a shared-memory atomic are not served in lane order (DESIGN.md §5,
  * K3).  Applies to the current device; 0 restores the default. */
 void ipls_debug_force_match_rank(int on);
-/* Test hook: how a level's terminal segments are processed.  0 (default): the last level
- * fused with the base case (k_term_fused) when the level's segments average
- * >= 32 Ki keys, else the separate terminal scatter + base-case kernels; 1: always fused;
- * 2: never fused.  Process-wide. */
+/* Test hook: how a level's terminal segments (every child <= base case) are processed.
+ * 0 (default): the child scatter fused with the warp base case (k_term_fused) when the
+ * level's segments average >= 32 Ki keys, else the child scatter and the base-case kernels
+ * separately; 1: always fused; 2: never fused; 3: the terminal segment sort -- windows of
+ * whole children of <= 16 Ki keys, a window scatter for segments of several windows, one CTA
+ * sorting each window into the user array (k_tss_scatter, k_win_sort; measured slower,
+ * DESIGN.md §5).  All four give identical records and final arrays.  Process-wide. */
 void ipls_debug_term_mode(int mode);
 /* Number of kernels the library enqueued since load (diagnostics / bench launch count). */
 uint64_t ipls_kernel_launch_count(void);

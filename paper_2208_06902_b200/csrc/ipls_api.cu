@@ -20,13 +20,14 @@
 
 #include "../../include/ipls.h"
 #include "ipls_kernels.cuh"
+#include "ipls_tss.cuh"
 
 using namespace ipls;
 
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
-std::atomic<int> g_term_mode{0};  // ipls_debug_term_mode: 0 auto, 1 always fused, 2 never
+std::atomic<int> g_term_mode{0};  // ipls_debug_term_mode: 0 auto, 1 k_term_fused, 2 separate, 3 window sort
 thread_local std::string g_last_cuda_error;
 
 struct CudaFail {
@@ -118,7 +119,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Params {
   uint64_t n;
   uint32_t k, B, chunk_keys;
-  uint32_t cap_segs, cap_chunks, cap_samples, cap_wins, cap_wbig, cap_fills;
+  uint32_t cap_segs, cap_chunks, cap_samples, cap_wins, cap_wbig, cap_fills, cap_twin;
   bool tree;  // IPLS_FLAG_TREE_MODEL: splitter-tree model instead of FMCD
 };
 
@@ -157,13 +158,16 @@ Params make_params(uint64_t n, uint32_t k, uint32_t B, bool tree = false) {
   p.cap_wins = (uint32_t)wins;
   p.cap_wbig = (uint32_t)wbig;
   p.cap_fills = (uint32_t)fills;
+  // terminal windows: a segment of m keys has <= ceil(m / (kTW - 4096)) of them
+  p.cap_twin = (uint32_t)std::min<uint64_t>(n / (kTW - 4096) + segs + 64, 0xffffffffull);
   return p;
 }
 
 // Fixed part of the workspace: scratch keys + descriptors of two levels + windows/fills of
 // two levels + counters.  The k-scaled per-level metadata is carved after it.
 struct FixedLayout {
-  size_t scratch, segs[2], chunks[2], wins[2], wbig[2], fills[2], ctr[2], err, tickets, total;
+  size_t scratch, segs[2], chunks[2], wins[2], wbig[2], fills[2], ctr[2], twins, twcur, err, tickets,
+      total;
 };
 
 FixedLayout fixed_layout(const Params& p) {
@@ -179,6 +183,8 @@ FixedLayout fixed_layout(const Params& p) {
     L.fills[i] = take((size_t)p.cap_fills * sizeof(Fill));
     L.ctr[i] = take(sizeof(LevelCounters));
   }
+  L.twins = take((size_t)p.cap_twin * sizeof(Window));
+  L.twcur = take((size_t)p.cap_twin * 4);
   L.err = take(16);
   L.tickets = take(64);
   L.total = o;
@@ -189,7 +195,7 @@ FixedLayout fixed_layout(const Params& p) {
 // allocation can be cleared cheaply.
 struct MetaLayout {
   size_t status, cflag, cref, chunk_pre, models, samples, seg_dst, seg_tot, seg_term, seg_done,
-      tree, total;
+      seg_tw, tree, total;
 };
 
 MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_t k,
@@ -207,6 +213,7 @@ MetaLayout meta_layout(uint64_t segs, uint64_t chunks, uint64_t samples, uint32_
   L.seg_tot = take(segs * k * 4);
   L.seg_term = take(segs * 4);
   L.seg_done = take(segs * 4);
+  L.seg_tw = take(segs * 8);
   L.tree = take(tree ? segs * kMaxK * 8 : 0);  // splitter heaps (8 KB per segment)
   L.total = o;
   return L;
@@ -293,6 +300,16 @@ void launch_scatter(uint32_t nchunk, cudaStream_t st, const LevelArgs& la, uint6
   ck_launch();
   }
   if (stable_only) return;
+  if (la.tss) {
+    // terminal segments of several windows: keys into their windows (k_win_sort after the level)
+    IPLS_PROF("tss_scatter", 0);
+    if (tree)
+      k_tss_scatter<F64, true><<<nchunk, kXThreads, tss_scatter_smem_bytes(), st>>>(la, user, scr);
+    else
+      k_tss_scatter<F64, false><<<nchunk, kXThreads, tss_scatter_smem_bytes(), st>>>(la, user, scr);
+    ck_launch();
+    return;
+  }
   if (la.fused_term) {
     // terminal chunks, each terminal segment base-sorted by the CTA that completes it
     IPLS_PROF("term_fused", 0);
@@ -375,7 +392,12 @@ void set_attrs() {
                             (int)fused_smem_bytes(kMaxK)));
     ck(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)win_scratch_bytes(kMaxK)));
+    ck(cudaFuncSetAttribute(tr ? k_tss_scatter<F64, true> : k_tss_scatter<F64, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)tss_scatter_smem_bytes()));
   }
+  ck(cudaFuncSetAttribute(k_win_sort<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)win_sort_smem_bytes()));
   done.insert(dev);
 }
 
@@ -621,6 +643,16 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     la.fused_term = (level_keys / std::max<uint32_t>(nseg, 1) >= 32768u) ? 1u : 0u;
     if (g_term_mode.load() == 1) la.fused_term = 1;
     if (g_term_mode.load() == 2) la.fused_term = 0;
+    // Terminal segments sorted by windows (ipls_tss.cuh) unless a test hook asks for the
+    // child scatter + base case (modes 1, 2).
+    // The terminal segment sort (ipls_tss.cuh) is a test-hook alternative: measured slower
+    // than the child scatter + warp base case on C1-C5 (rejected round 2).
+    la.tss = (g_term_mode.load() == 3) ? 1u : 0u;
+    if (la.tss) la.fused_term = 0;
+    la.seg_tw = at<uint2>(meta, ML.seg_tw);
+    la.twins = at<Window>(fixed, FL.twins);
+    la.twcur = at<uint32_t>(fixed, FL.twcur);
+    la.cap_twin = p.cap_twin;
     la.ticket = &cctr->ticket;
     la.status = at<uint64_t>(meta, ML.status);
     la.cflag = at<uint8_t>(meta, ML.cflag);
@@ -698,9 +730,23 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     const LevelCounters c = h_ctr[0];
     const uint32_t herr = h_ctr[1].err;
     prof_add_bytes("scatter", 16.0 * c.term_keys);  // the base case done inside k_term_fused
+    prof_add_bytes("tss_scatter", 16.0 * c.tsplit_keys);
     if (herr & kErrNan) return IPLS_ERR_NAN_KEY;
     if (herr & kErrOverflow) return IPLS_ERR_OUT_OF_MEMORY;
 
+    // terminal segments: one CTA sorts each window into the user array
+    if (c.n_twin) {
+      IPLS_PROF("win_sort", 16.0 * c.twin_keys);
+      k_win_sort<F64><<<c.n_twin, kWSThreads, win_sort_smem_bytes(), st>>>(
+          at<Window>(fixed, FL.twins), keys, scr, d_err);
+      ck_launch();
+      if (trace && trace->tr->d_snapshots && iter < trace->tr->snapshot_levels) {
+        // the level's image of a terminal segment: its sorted keys (each child's multiset)
+        uint64_t* snap = static_cast<uint64_t*>(trace->tr->d_snapshots) + (size_t)iter * n;
+        k_snapshot_term<<<nseg, 256, 0, st>>>(segs, la.seg_term, keys, snap);
+        ck_launch();
+      }
+    }
     // base case of this level's base children, fills of its homogeneous children
     if (c.n_windows) {
       IPLS_PROF("base_warp", 16.0 * c.win_keys);

@@ -64,6 +64,9 @@ struct LevelCounters {      // device-side counters of the level being built
   uint32_t n_redo;          // this level's segments k_fit_small left to k_gather_fit
   uint32_t sticket;         // chunk tickets of k_term_fused (next level's struct, zeroed)
   uint64_t term_keys;       // keys base-sorted inside k_term_fused
+  uint32_t n_twin, n_twin_split;  // terminal windows (k_win_sort); those of split segments
+  uint64_t twin_keys;       // keys in terminal windows
+  uint64_t tsplit_keys;     // keys of terminal segments scattered into windows (k_tss_scatter)
 };
 
 constexpr uint32_t kErrNan = 1u;

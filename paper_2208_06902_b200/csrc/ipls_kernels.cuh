@@ -57,6 +57,17 @@ constexpr size_t kWBSmemPerWarp = (size_t)2 * kWBStride * 8 + (size_t)kWBBinWord
 __device__ __forceinline__ uint32_t wb_phys(uint32_t f) { return f + ((f >> 5) << 2); }
 constexpr uint32_t kFineOverflow = 32;          // fine-bin load that triggers the bitonic fallback
 
+// Terminal segment sort (k_tss_scatter + k_win_sort, ipls_tss.cuh): a terminal segment is cut
+// into windows of whole children of <= kTW keys; a window of W' = kTW - (largest child)
+// positions starts at the first child starting in [g W', (g+1) W'), so every window holds
+// <= kTW keys and child c lies in window floor(start(c) / W').
+#ifndef IPLS_TW
+#define IPLS_TW 16384
+#endif
+constexpr uint32_t kTW = IPLS_TW;
+static_assert(kTW >= 8192 && kTW <= 32768, "W' and the window sort's u16 bin starts fit 16 bits");
+constexpr uint32_t kTWMaxWin = (uint32_t)(((uint64_t)1024 * 4096 + (kTW - 4096) - 1) / (kTW - 4096)) + 2;
+
 // ------------------------------------------------------------------------------------
 // Block-wide exact sort of n <= cap ordering keys in smem (used for samples and base-case
 // windows).  A 256-way coarse histogram of (ok - min) >> shift allots each coarse bin as
@@ -699,6 +710,11 @@ struct LevelArgs {
   uint64_t* cref;        // [chunk][k] the chunk's value of a one-value bucket
   uint32_t* seg_term;    // [seg]      1: every child <= base case (terminal segment)
   uint32_t* seg_done;    // [seg]      chunks of the segment scattered (k_term_fused)
+  uint32_t tss;          // terminal segments: window scatter + window sort (k_tss_scatter, k_win_sort)
+  uint2* seg_tw;         // [seg]      {first terminal window, W'} (W' = 0: the segment is one window)
+  Window* twins;         // terminal windows of the level (k_win_sort)
+  uint32_t* twcur;       // [window]   k_tss_scatter's fill cursor
+  uint32_t cap_twin;
   uint32_t epoch;
   uint32_t* err;
   int check_nan;
@@ -899,9 +915,11 @@ __device__ void segment_bases(const LevelArgs& a, uint32_t s, const SegDesc& sg,
   for (int q = 0; q < kCBpt; ++q) x += tot[q];
   uint32_t ex = block_exclusive_scan<kCThreads>(x, os.warp, nullptr);
   const uint32_t dstbuf = a.dstbuf;  // 1 = scratch, 0 = user array
+  uint32_t cst[kCBpt];               // child starts inside the segment
 #pragma unroll
   for (int q = 0; q < kCBpt; ++q) {
     const uint32_t b = threadIdx.x * kCBpt + q;
+    cst[q] = ex;
     if (b < k) {
       const uint64_t enc = a.single_offsets ? (uint64_t)ex
                                             : ((dstbuf == 0 ? kDstUserBit : 0ull) | (sg.begin + ex));
@@ -919,6 +937,58 @@ __device__ void segment_bases(const LevelArgs& a, uint32_t s, const SegDesc& sg,
   for (int q = 0; q < kCBpt; ++q) big |= tot[q] > a.base_case;
   const int any_big = __syncthreads_or(big);
   if (threadIdx.x == 0) a.seg_term[s] = (!a.single_offsets && !any_big) ? 1u : 0u;
+  if (!a.tss || a.single_offsets || any_big) return;  // block-uniform
+  // ---- terminal segment sort: windows of whole children (kTW, above) ----
+  __shared__ uint32_t s_bnd[kTWMaxWin];
+  __shared__ uint32_t s_mc, s_last, s_first;
+  uint32_t mc = 0, last = 0;  // largest child, start of the last non-empty child
+#pragma unroll
+  for (int q = 0; q < kCBpt; ++q) {
+    mc = max(mc, tot[q]);
+    if (tot[q]) last = max(last, cst[q]);
+  }
+  if (threadIdx.x == 0) { s_mc = 0; s_last = 0; }
+  __syncthreads();
+  if (mc) atomicMax(&s_mc, mc);
+  if (last) atomicMax(&s_last, last);
+  __syncthreads();
+  const uint32_t m = sg.m;
+  const uint32_t Wp = (m <= kTW) ? 0u : kTW - s_mc;   // s_mc <= base case <= 4096 < kTW / 2
+  // window g holds the children starting in [g W', (g+1) W'): none of these intervals is
+  // empty up to the one holding the last child's start (no child is longer than W')
+  const uint32_t G = Wp ? s_last / Wp + 1 : 1u;
+  for (uint32_t g = threadIdx.x; g < G; g += kCThreads) s_bnd[g] = ~0u;
+  __syncthreads();
+  if (Wp) {
+#pragma unroll
+    for (int q = 0; q < kCBpt; ++q)
+      if (tot[q]) atomicMin(&s_bnd[cst[q] / Wp], cst[q]);
+  } else if (threadIdx.x == 0) {
+    s_bnd[0] = 0;
+  }
+  if (threadIdx.x == 0) {
+    s_first = atomicAdd(&a.nctr->n_twin, G);
+    atomicAdd((unsigned long long*)&a.nctr->twin_keys, (unsigned long long)m);
+    if (Wp) {
+      atomicAdd(&a.nctr->n_twin_split, G);
+      atomicAdd((unsigned long long*)&a.nctr->tsplit_keys, (unsigned long long)m);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) a.seg_tw[s] = make_uint2(s_first, Wp | (G << 16));
+  for (uint32_t g = threadIdx.x; g < G; g += kCThreads) {
+    const uint32_t gi = s_first + g;
+    if (gi < a.cap_twin) {
+      Window wv;
+      wv.begin = sg.begin + s_bnd[g];
+      wv.len = (g + 1 < G ? s_bnd[g + 1] : m) - s_bnd[g];
+      wv.buf = Wp ? dstbuf : 1u - dstbuf;  // a one-window segment is sorted where it lies
+      a.twins[gi] = wv;
+      a.twcur[gi] = 0;
+    } else {
+      atomicOr(a.err, kErrOverflow);
+    }
+  }
 }
 
 // Per segment, after its last chunk has been scattered (run by that CTA): child classes with
@@ -1774,7 +1844,7 @@ __global__ __launch_bounds__(kEThreads) void k_emit(LevelArgs a) {
   __shared__ OffSmem os;
   if (*((volatile const uint32_t*)a.err) & kErrNan) return;
   const uint32_t s = blockIdx.x;
-  if (a.fused_term && a.seg_term[s]) return;  // k_term_fused packed and sorted its children
+  if ((a.fused_term || a.tss) && a.seg_term[s]) return;  // k_term_fused / the window sort own them
   const SegDesc sg = a.segs[s];
   const ModelDev md = a.models[s];
   segment_emit<kEThreads>(a, s, sg, md, os, reinterpret_cast<uint32_t*>(smraw));
@@ -2559,6 +2629,15 @@ __global__ void k_snapshot(const SegDesc* __restrict__ segs, const uint64_t* __r
   const SegDesc sg = segs[blockIdx.x];
   const uint64_t* s = (dstbuf ? scr : user) + sg.begin;
   for (uint32_t i = threadIdx.x; i < sg.m; i += blockDim.x) snap[sg.begin + i] = s[i];
+}
+
+// Trace only: a terminal segment's image after its level is its sorted keys (k_win_sort's
+// output in the user array): every child holds its multiset there.
+__global__ void k_snapshot_term(const SegDesc* __restrict__ segs, const uint32_t* __restrict__ seg_term,
+                                const uint64_t* __restrict__ user, uint64_t* __restrict__ snap) {
+  if (!seg_term[blockIdx.x]) return;
+  const SegDesc sg = segs[blockIdx.x];
+  for (uint32_t i = threadIdx.x; i < sg.m; i += blockDim.x) snap[sg.begin + i] = user[sg.begin + i];
 }
 
 // ipls_regroup_runs: move pieces (src offset, dst offset, length) of keys, one warp per piece,

@@ -649,7 +649,7 @@ def test_configs_full_size_layout_after_every_level(ipls, name):
     torch.cuda.empty_cache()
 
 
-@pytest.fixture(params=[1, 2], ids=["fused", "separate"])
+@pytest.fixture(params=[1, 2, 3], ids=["fused", "separate", "windows"])
 def term_mode(ipls, request):
     ipls.lib().ipls_debug_term_mode(request.param)
     yield request.param
