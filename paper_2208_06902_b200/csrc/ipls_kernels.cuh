@@ -1752,19 +1752,25 @@ __device__ void scatter_term_chunk(const LevelArgs& a, uint64_t* __restrict__ ds
       v[r] = (i < tl) ? slot[h + i] : 0ull;
       bk[r] = (i < tl) ? bucket(v[r]) : 0xffffffffu;
     }
+    // The count's return value is the key's rank among the tile's keys of its bucket (the
+    // order inside a terminal child is free, R11): bk = bucket | rank << 16.
     if (!dense) {
 #pragma unroll
       for (int r = 0; r < kTItems; ++r)
-        if (bk[r] != 0xffffffffu) atomicAdd(&cnt[bk[r]], 1u);
+        if (bk[r] != 0xffffffffu) bk[r] |= atomicAdd(&cnt[bk[r]], 1u) << 16;
     } else {
 #pragma unroll
       for (int r = 0; r < kTItems; ++r) {
         const uint32_t b0 = __shfl_sync(0xffffffffu, bk[r], 0);
         if (__all_sync(0xffffffffu, bk[r] == b0 || bk[r] == 0xffffffffu)) {
+          // valid lanes are a prefix of the warp (the tile's tail is its last keys)
           const uint32_t nv = __popc(__ballot_sync(0xffffffffu, bk[r] != 0xffffffffu));
-          if (lane == 0 && nv) atomicAdd(&cnt[b0], nv);
+          uint32_t base = 0;
+          if (lane == 0 && nv) base = atomicAdd(&cnt[b0], nv);
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (bk[r] != 0xffffffffu) bk[r] |= (base + (uint32_t)lane) << 16;
         } else if (bk[r] != 0xffffffffu) {
-          atomicAdd(&cnt[bk[r]], 1u);
+          bk[r] |= atomicAdd(&cnt[bk[r]], 1u) << 16;
         }
       }
     }
@@ -1793,28 +1799,9 @@ __device__ void scatter_term_chunk(const LevelArgs& a, uint64_t* __restrict__ ds
     dense = (uint32_t)__syncthreads_count(cc != 0) * 32u <= tl;
     SC_TICK(5);
     // ---- (C) placement into the slot (every thread holds its keys in registers) ----
-    if (!dense) {
-#pragma unroll
-      for (int r = 0; r < kTItems; ++r)
-        if (bk[r] != 0xffffffffu) bk[r] = atomicAdd(&cur[bk[r]], 1u);
-    } else {
-#pragma unroll
-      for (int r = 0; r < kTItems; ++r) {
-        const uint32_t b0 = __shfl_sync(0xffffffffu, bk[r], 0);
-        if (__all_sync(0xffffffffu, bk[r] == b0 || bk[r] == 0xffffffffu)) {
-          const uint32_t nv = __popc(__ballot_sync(0xffffffffu, bk[r] != 0xffffffffu));
-          uint32_t base = 0;
-          if (lane == 0 && nv) base = atomicAdd(&cur[b0], nv);
-          if (bk[r] != 0xffffffffu) bk[r] = __shfl_sync(0xffffffffu, base, 0) + lane;
-          else __shfl_sync(0xffffffffu, base, 0);
-        } else if (bk[r] != 0xffffffffu) {
-          bk[r] = atomicAdd(&cur[bk[r]], 1u);
-        }
-      }
-    }
 #pragma unroll
     for (int r = 0; r < kTItems; ++r)
-      if (r * NT + t < tl) slot[bk[r]] = v[r];
+      if (r * NT + t < tl) slot[cur[bk[r] & 0xffffu] + (bk[r] >> 16)] = v[r];
     __syncthreads();
     SC_TICK(6);
     // ---- (D) write-out ----
