@@ -1421,7 +1421,9 @@ __device__ void scatter_stable_chunk(const LevelArgs& a, uint64_t* __restrict__ 
                                      const ChunkDesc& ch, const ModelDev& md,
                                      unsigned char* smraw) {
   constexpr int NT = kSThreads;
-  constexpr bool kStageBucket = MODE == (int)kModelTree;  // a tree descent costs more than a load
+  // the write-out reads each staged key's bucket (u16) instead of recomputing it: the FP64
+  // model chain sits on the write-out's critical path (C2 -3 %, C3 -5 % on this kernel)
+  constexpr bool kStageBucket = true;
   const uint32_t k = a.k;
   uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);              // kSTile keys
   uint16_t* sbk = reinterpret_cast<uint16_t*>(stage + kSTile);        // kSTile (tree only)

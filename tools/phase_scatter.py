@@ -37,3 +37,4 @@ print(f"terminal scatter: {ph[29]} tiles; cycles per tile (thread 0): slots {ph[
 print(f"large-sample fit (1 CTA, cycles): gather {ph[16]} sort {ph[17]} fmcd {ph[18]}")
 print("fit cycle sums over all CTAs of the last sort (x1e6): gather", ph[8] / 1e6, "sort", ph[9] / 1e6,
       "fmcd", ph[10] / 1e6)
+print("all phase counters:", [int(x) for x in ph])
