@@ -36,7 +36,8 @@ constexpr uint32_t kMaxK = 1024;
 constexpr int kBCThreads = 512;
 constexpr int kBCItems = 8;
 constexpr int kBigCap = kBCThreads * kBCItems;  // 4096 = the largest base child
-constexpr size_t kBCSmem = (size_t)kBigCap * 8 + (size_t)kBigCap * 4;
+// keys + fine-bin words (4 pad words per 32: each thread's 8 bins are 2 conflict-free uint4)
+constexpr size_t kBCSmem = (size_t)kBigCap * 8 + (size_t)(kBigCap + kBigCap / 8) * 4;
 
 // small-window base case (k_base_warp)
 constexpr int kWBCap = 256;                      // keys per warp window
@@ -1964,7 +1965,7 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
   if (lane == 0) { ss.red[wp] = mn; ss.red[NW + wp] = mx; }
   for (uint32_t c = threadIdx.x; c < 256; c += NT) ss.cinfo[c] = 0u;
   {
-    uint4* f4 = reinterpret_cast<uint4*>(fh) + threadIdx.x * (ITEMS / 4);
+    uint4* f4 = reinterpret_cast<uint4*>(fh + wb_phys(threadIdx.x * ITEMS));
 #pragma unroll
     for (int q = 0; q < ITEMS / 4; ++q) f4[q] = make_uint4(0, 0, 0, 0);
   }
@@ -2004,13 +2005,15 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
   }
   __syncthreads();
   BASE_TICK(4);
-  uint32_t fs[ITEMS];  // fine bin
+  // fine bin f's count is fh[wb_phys(f)]; the atomic returns the key's arrival rank in its
+  // bin, so the placement needs no second atomic
+  uint32_t fs[ITEMS];  // fine bin | rank << 16
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     fs[j] = 0;
     if (j * NT + threadIdx.x < len) {
-      fs[j] = base_fine_bin(v[j], sh, ss.cinfo);
-      atomicAdd(&fh[fs[j]], 1u);
+      const uint32_t f = base_fine_bin(v[j], sh, ss.cinfo);
+      fs[j] = f | (atomicAdd(&fh[wb_phys(f)], 1u) << 16);
     }
   }
   __syncthreads();
@@ -2018,7 +2021,7 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
   // exclusive scan of the NT*ITEMS fine-bin counts: thread t owns bins [ITEMS t, ITEMS t + ITEMS)
   uint32_t mxc = 0, lo, hi;  // this thread's fine bins hold B[lo, hi) after placement
   {
-    uint4* f4 = reinterpret_cast<uint4*>(fh) + threadIdx.x * (ITEMS / 4);
+    uint4* f4 = reinterpret_cast<uint4*>(fh + wb_phys(threadIdx.x * ITEMS));
     uint32_t sum = 0;
 #pragma unroll
     for (int q = 0; q < ITEMS / 4; ++q) {
@@ -2048,13 +2051,13 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
     // of different keys send the window to the bitonic fallback.
     constexpr uint32_t NB = NT * ITEMS;
     auto big_start = [&](uint32_t f) -> uint32_t {  // start of bin f if it is big, else ~0
-      const uint32_t st = fh[f], en = f + 1 < NB ? fh[f + 1] : len;
+      const uint32_t st = fh[wb_phys(f)], en = f + 1 < NB ? fh[wb_phys(f + 1)] : len;
       return en - st > kFineOverflow ? st : ~0u;
     };
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j)
       if (j * NT + threadIdx.x < len) {
-        const uint32_t st = big_start(fs[j]);
+        const uint32_t st = big_start(fs[j] & 0xffffu);
         if (st != ~0u) B[st] = v[j];
       }
     __syncthreads();
@@ -2062,7 +2065,7 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j)
       if (j * NT + threadIdx.x < len) {
-        const uint32_t st = big_start(fs[j]);
+        const uint32_t st = big_start(fs[j] & 0xffffu);
         if (st != ~0u && B[st] != v[j]) mixed = true;
       }
     if (__syncthreads_or(mixed)) {
@@ -2076,17 +2079,19 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     if (j * NT + threadIdx.x < len) {
-      B[atomicAdd(&fh[fs[j]], 1u)] = v[j];
+      B[fh[wb_phys(fs[j] & 0xffffu)] + (fs[j] >> 16)] = v[j];
     }
   }
   __syncthreads();
   BASE_TICK(7);
-  // fine bin f occupies B[f ? fh[f - 1] : 0, fh[f]) now.
+  // fine bin f occupies B[fh[wb_phys(f)], fh[wb_phys(f + 1)]) (the last one ends at len).
+  constexpr uint32_t NBF = NT * ITEMS;
+  auto bin_end = [&](uint32_t f) -> uint32_t { return f + 1 < NBF ? fh[wb_phys(f + 1)] : len; };
   uint32_t big = 0;  // this thread's fine bins above kFineOverflow keys (one value each)
   if (overflow) {
     uint32_t e0 = lo;
     for (int q = 0; q < ITEMS; ++q) {
-      const uint32_t e1 = fh[threadIdx.x * ITEMS + q];
+      const uint32_t e1 = bin_end(threadIdx.x * ITEMS + q);
       big |= (e1 - e0 > kFineOverflow ? 1u : 0u) << q;
       e0 = e1;
     }
@@ -2101,8 +2106,8 @@ __device__ uint64_t* sort_regs_to_smem(uint64_t (&v)[ITEMS], uint32_t len, uint6
     uint32_t s1 = hi, nxt = 0;
     if (msk) {
       const uint32_t f = threadIdx.x * ITEMS + (__ffs(msk) - 1);
-      s1 = f ? fh[f - 1] : 0u;
-      nxt = fh[f];
+      s1 = fh[wb_phys(f)];
+      nxt = bin_end(f);
     }
     if (s0 + 1 < s1) {
       uint64_t* q = B + s0;  // q[1] is the key being inserted
