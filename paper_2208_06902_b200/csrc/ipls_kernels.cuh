@@ -1422,9 +1422,7 @@ __device__ void scatter_stable_chunk(const LevelArgs& a, uint64_t* __restrict__ 
                                      const ChunkDesc& ch, const ModelDev& md,
                                      unsigned char* smraw) {
   constexpr int NT = kSThreads;
-  // the write-out reads each staged key's bucket (u16) instead of recomputing it: the FP64
-  // model chain sits on the write-out's critical path (C2 -3 %, C3 -5 % on this kernel)
-  constexpr bool kStageBucket = true;
+  constexpr bool kStageBucket = MODE == (int)kModelTree;  // a tree descent costs more than a load
   const uint32_t k = a.k;
   uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);              // kSTile keys
   uint16_t* sbk = reinterpret_cast<uint16_t*>(stage + kSTile);        // kSTile (tree only)
@@ -1668,20 +1666,20 @@ __device__ void scatter_stable_chunk(const LevelArgs& a, uint64_t* __restrict__ 
 }
 
 // Terminal chunks (k_scatter_term): 1024 threads (32 warps, 1 CTA per SM), tiles of 8192 keys
-// streamed through a ring of kTRing smem slots by TMA bulk copies issued one tile ahead, so
-// keys never wait in prefetch registers.  A slot doubles as its tile's stage: (A) keys to
-// registers + count per bucket (the atomic's return value is the key's rank in its bucket),
-// (B) run starts, (C) placement at run start + rank into the same slot, with the bucket
-// staged as a u16 beside it, (D) write-out reading the staged bucket.  No warp counters, no
-// homogeneity (terminal segments have no child above the base case).
+// streamed through a ring of kTRing smem slots by TMA bulk copies issued two tiles ahead, so
+// no load latency is exposed inside a chunk and keys never wait in prefetch registers.  A
+// slot doubles as its tile's stage: (A) keys to registers + count per bucket, (B) run starts,
+// (C) placement by an atomic cursor per bucket into the same slot, (D) write-out with the
+// bucket recomputed from the staged key.  No warp counters, no homogeneity (terminal
+// segments have no child above the base case).
 constexpr int kTThreads = 1024;
 constexpr int kTItems = 8;
 constexpr int kTTile = kTThreads * kTItems;   // 8192
-constexpr int kTRing = 2;  // 2 slots + a staged u16 bucket per key (3 slots and recomputed buckets: +2.5 %)
+constexpr int kTRing = 3;
 constexpr int kTSlot = kTTile + 4;            // keys per slot (+ parity shift, 32-byte multiple)
 
 __host__ __device__ constexpr size_t scatter_term_smem_bytes(uint32_t k) {
-  return (size_t)kTRing * kTSlot * 8 + (size_t)k * 4 * 4 + (size_t)kTTile * 2 + 64;
+  return (size_t)kTRing * kTSlot * 8 + (size_t)k * 4 * 4 + 64;
 }
 
 // Tile [t0, t0 + tl) of a chunk starting at p (h = parity of its start): the keys land at
@@ -1715,7 +1713,6 @@ __device__ void scatter_term_chunk(const LevelArgs& a, uint64_t* __restrict__ ds
   uint32_t* cur = cnt + k;                                          // k: placement cursor
   uint32_t* runo = cur + k;                                         // k
   uint32_t* adjo = runo + k;                                        // k
-  uint16_t* sbk = reinterpret_cast<uint16_t*>(adjo + k);            // kTTile: staged buckets
   __shared__ uint32_t s_warp[2][32];
   __shared__ __align__(8) uint64_t s_bar[kTRing];
   const Bucketer<F64, MODE> bucket(md, k);
@@ -1805,11 +1802,7 @@ __device__ void scatter_term_chunk(const LevelArgs& a, uint64_t* __restrict__ ds
     // ---- (C) placement into the slot (every thread holds its keys in registers) ----
 #pragma unroll
     for (int r = 0; r < kTItems; ++r)
-      if (r * NT + t < tl) {
-        const uint32_t q = cur[bk[r] & 0xffffu] + (bk[r] >> 16);
-        slot[q] = v[r];
-        sbk[q] = (uint16_t)(bk[r] & 0xffffu);
-      }
+      if (r * NT + t < tl) slot[cur[bk[r] & 0xffffu] + (bk[r] >> 16)] = v[r];
     __syncthreads();
     SC_TICK(6);
     // ---- (D) write-out ----
@@ -1819,7 +1812,7 @@ __device__ void scatter_term_chunk(const LevelArgs& a, uint64_t* __restrict__ ds
       v[r] = (q < tl) ? slot[q] : 0ull;
     }
 #pragma unroll
-    for (int r = 0; r < kTItems; ++r) bk[r] = adjo[sbk[min(r * NT + t, tl - 1)]];
+    for (int r = 0; r < kTItems; ++r) bk[r] = adjo[bucket(v[r])];
 #pragma unroll
     for (int r = 0; r < kTItems; ++r) {
       const uint32_t q = r * NT + t;
