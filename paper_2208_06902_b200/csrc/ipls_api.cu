@@ -127,7 +127,7 @@ struct Params {
 #define IPLS_CHUNK_CAP 114688  // 112 Ki: C5 -0.6 % against 96 Ki (interleaved A/B; C2-C4 unchanged)
 #endif
 uint32_t pick_chunk_keys(uint64_t n) {
-  // ~8 chunks per SM at level 0 (148 SMs), 4096..98304 keys; from 16384 keys up a multiple of
+  // ~8 chunks per SM at level 0 (148 SMs), 4096..IPLS_CHUNK_CAP keys; from 16384 keys up a multiple of
   // the terminal scatter's 16384-key tile.  Larger chunks amortise each chunk's k-wide
   // lookback, histogram and run setup (98304 keys: C2 -1.2 %, C5 -1.2 % against 65536).
   uint64_t c = n / (148 * 8);
