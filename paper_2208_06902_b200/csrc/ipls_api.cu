@@ -640,7 +640,12 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     // base-case pass (its packing runs inside the completing CTA): levels whose segments
     // average >= 32 Ki keys (C2-C5 level 1); small segments (level 2 of C3/C5) keep the
     // separate kernels, whose emit runs 4 CTAs per SM.
-    la.fused_term = (level_keys / std::max<uint32_t>(nseg, 1) >= 32768u) ? 1u : 0u;
+    // and whose segments are all <= 2^20 keys (the level's largest sample is S(2^20)): with
+    // larger segments (skewed inputs: C3, C5, the paper's mixture and Zipf) the fused kernel's
+    // per-CTA base-case phases balance worse than the separate launches (C3 -1.2 %, C5 -1.4 %,
+    // mixture -2.7 %, Zipf -2.8 % separate; C2 -2.1 % fused)
+    la.fused_term = (level_keys / std::max<uint32_t>(nseg, 1) >= 32768u &&
+                     max_S <= sample_size(1ull << 20, k)) ? 1u : 0u;
     if (g_term_mode.load() == 1) la.fused_term = 1;
     if (g_term_mode.load() == 2) la.fused_term = 0;
     // Terminal segments sorted by windows (ipls_tss.cuh) unless a test hook asks for the
