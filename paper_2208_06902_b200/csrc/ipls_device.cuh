@@ -165,6 +165,17 @@ __device__ __forceinline__ void st_evict_last(uint64_t* p, uint64_t v) {
   asm volatile("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
                " st.global.L2::cache_hint.b64 [%0], %1, pol;\n}" ::"l"(p), "l"(v) : "memory");
 }
+// 8- / 16-byte global -> shared copies completed by the issuing thread's cp.async groups
+// (the window descriptors and the unaligned head/tail keys of the base case, fetched one
+// window ahead so that their latency is not exposed)
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -1705,7 +1705,8 @@ __device__ __forceinline__ void tile_issue(uint64_t* slot, const uint64_t* p, ui
 template <bool F64, int MODE>
 __device__ void scatter_term_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_user,
                                    uint64_t* __restrict__ dst_scr, uint32_t c,
-                                   const ChunkDesc& ch, const ModelDev& md, unsigned char* smraw) {
+                                   const ChunkDesc& ch, const ModelDev& md, unsigned char* smraw,
+                                   uint32_t* next_ticket = nullptr) {
   constexpr int NT = kTThreads;
   const uint32_t k = a.k;
   uint64_t* slots = reinterpret_cast<uint64_t*>(smraw);            // kTRing x kTSlot
@@ -1731,6 +1732,8 @@ __device__ void scatter_term_chunk(const LevelArgs& a, uint64_t* __restrict__ ds
     for (uint32_t j = 0; j < min(ntile, (uint32_t)kTRing - 1); ++j)
       tile_issue(slots + j * kTSlot, p, h, j * kTTile, min((uint32_t)kTTile, ch.len - j * kTTile),
                  room - j * kTTile, &s_bar[j]);
+    // k_term_fused: the next chunk's ticket, while the first tiles load
+    if (next_ticket) *next_ticket = atomicAdd(&a.nctr->sticket, 1u);
   }
   const uint64_t pol = policy_evict_last();
   __syncthreads();
@@ -2230,18 +2233,22 @@ __device__ void warp_bitonic_ok(uint64_t* B, uint32_t len, int lane) {
 // One warp sorts the windows first, first + stride, ... < nwin of `wins` (its smem region:
 // IN, bins; its two mbarriers, initialised by the caller; it_base: the number of windows the
 // warp has taken through these mbarriers so far, which fixes their phase).
-template <bool F64>
+template <bool F64, bool WSMEM>
 __device__ void base_warp_windows(const Window* __restrict__ wins, uint32_t first, uint32_t nwin,
                                   uint32_t stride, uint64_t* __restrict__ user,
                                   const uint64_t* __restrict__ scr, uint64_t* IN, uint32_t* bins,
-                                  uint64_t* mbar, uint32_t& it_base) {
+                                  uint64_t* mbar, Window* dring, uint32_t& it_base) {
   const int lane = threadIdx.x & 31;
   const uint32_t gw = first, gstride = stride;
-  // lane 0: start the bulk copy of the window described by wv into IN[b].  Descriptors are
-  // loaded two windows ahead so that their global latency is off the critical path.
+  // lane 0: start the copies of window wv into IN[b]: its 16-byte-aligned body by a TMA bulk
+  // copy (mbar[b]), the 0-1 keys before and after it (head, tail) by 8-byte cp.async into the
+  // slots around the body (lane 0's cp.async group of this iteration, complete by the next)
   auto issue = [&](const Window& wv, int b) {
     const uint64_t* g = (wv.buf ? scr : user) + wv.begin;
     const WinGeom gm = win_geom(g, wv.len);
+    uint64_t* K = IN + (size_t)b * kWBStride + 2 - gm.head;
+    if (gm.head) cp_async8(K, g);
+    if (gm.tail) cp_async8(K + wv.len - 1, g + wv.len - 1);
     if (gm.body) {
       mbar_arrive_tx(&mbar[b], gm.body * 8u);
       bulk_g2s(IN + (size_t)b * kWBStride + 2, g + gm.head, gm.body * 8u, &mbar[b]);
@@ -2256,23 +2263,41 @@ __device__ void base_warp_windows(const Window* __restrict__ wins, uint32_t firs
 #else
 #define WB_TICK(N)
 #endif
-  Window d_cur{}, d_nxt{};  // lane 0: descriptors of windows cur and cur+1 (in flight)
-  if (lane == 0) {
-    if (gw < nwin) { d_cur = wins[gw]; issue(d_cur, it_base & 1); }
-    if (gw + gstride < nwin) d_nxt = wins[gw + gstride];
-  }
+  // Descriptors: WSMEM (k_term_fused's window list in shared memory) are read in place;
+  // global ones go through a per-warp ring of 4 smem slots, fetched by cp.async two windows
+  // ahead (slot it & 3: the current window, it + 1: the one being issued, it + 2: in flight),
+  // so no lane holds descriptors in registers.
   uint32_t it = it_base;
+  if (lane == 0 && gw < nwin) {
+    Window w0;
+    if constexpr (WSMEM) {
+      w0 = wins[gw];
+    } else {
+      w0 = wins[gw];
+      dring[it & 3] = w0;
+      if (gw + gstride < nwin) cp_async16(&dring[(it + 1) & 3], &wins[gw + gstride]);
+    }
+    issue(w0, it & 1);
+    cp_async_commit();
+  }
   for (uint32_t cur = gw; cur < nwin; ++it, cur += gstride) {
     const int b = it & 1;
-    Window wv;
-    wv.begin = __shfl_sync(0xffffffffu, d_cur.begin, 0);
-    wv.len = __shfl_sync(0xffffffffu, d_cur.len, 0);
-    wv.buf = __shfl_sync(0xffffffffu, d_cur.buf, 0);
     if (lane == 0) {
-      d_cur = d_nxt;  // loaded one window ago
-      if (cur + gstride < nwin) issue(d_cur, b ^ 1);
-      if (cur + 2 * gstride < nwin) d_nxt = wins[cur + 2 * gstride];  // consumed next window
+      cp_async_wait_all();  // head/tail of window cur, descriptor of cur + stride
+      if (cur + gstride < nwin) {
+        if constexpr (WSMEM) {
+          issue(wins[cur + gstride], b ^ 1);
+        } else {
+          issue(dring[(it + 1) & 3], b ^ 1);
+          if (cur + 2 * gstride < nwin) cp_async16(&dring[(it + 2) & 3], &wins[cur + 2 * gstride]);
+        }
+      }
+      cp_async_commit();
     }
+    __syncwarp();
+    Window wv;
+    if constexpr (WSMEM) wv = wins[cur];
+    else wv = dring[it & 3];
     WB_TICK(0);
     const uint32_t len = wv.len;
     const uint64_t* src = (wv.buf ? scr : user) + wv.begin;
@@ -2281,8 +2306,6 @@ __device__ void base_warp_windows(const Window* __restrict__ wins, uint32_t firs
     uint64_t* INb = IN + (size_t)b * kWBStride;
     uint64_t* K = INb + 2 - gm.head;  // key i of the window
     uint64_t* B = INb;                // placement array once the keys are in registers
-    if (lane == 0 && gm.head) K[0] = __ldcs(src);
-    if (lane == 1 && gm.tail) K[len - 1] = __ldcs(src + len - 1);
     mbar_wait(&mbar[b], (it >> 1) & 1);
     __syncwarp();
     // Slots past the end hold a copy of key 0 so that the bounds need no predicate.
@@ -2489,6 +2512,7 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
     const uint64_t* __restrict__ scr) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ uint64_t s_mbar[kWBWarps][2];
+  __shared__ __align__(16) Window s_dring[kWBWarps][4];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   uint64_t* IN = reinterpret_cast<uint64_t*>(smraw + wp * kWBSmemPerWarp);  // 2 x kWBStride
   uint32_t* bins = reinterpret_cast<uint32_t*>(IN + 2 * kWBStride);          // kWBBinWords
@@ -2500,8 +2524,8 @@ __global__ __launch_bounds__(kWBWarps * 32, 1) void k_base_warp(
   }
   __syncwarp();
   uint32_t it = 0;
-  base_warp_windows<F64>(wins, blockIdx.x * kWBWarps + wp, nwin, gridDim.x * kWBWarps, user, scr,
-                         IN, bins, mbar, it);
+  base_warp_windows<F64, false>(wins, blockIdx.x * kWBWarps + wp, nwin, gridDim.x * kWBWarps, user,
+                                scr, IN, bins, mbar, s_dring[wp], it);
 }
 
 // ------------------------------------------------------------------------------------
@@ -2531,7 +2555,7 @@ __global__ __launch_bounds__(kTThreads, 1) void k_term_fused(LevelArgs a, uint64
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ uint64_t s_mbar[kWBWarps][2];
   __shared__ OffSmem os;
-  __shared__ uint32_t s_ticket, s_last, s_nw;
+  __shared__ uint32_t s_ticket[2], s_last, s_nw;
   __shared__ uint64_t s_keys;
   const uint32_t t = threadIdx.x;
   const int lane = t & 31, wp = t >> 5;
@@ -2546,29 +2570,37 @@ __global__ __launch_bounds__(kTThreads, 1) void k_term_fused(LevelArgs a, uint64
   uint32_t it_base = 0;  // windows this warp has sorted (mbarrier phase)
   const uint32_t k = a.k;
   if (*((volatile const uint32_t*)a.err) & kErrNan) return;
-  while (true) {
+  // Chunk tickets are taken one chunk ahead (s_ticket[ip & 1] is this chunk's, thread 0 fills
+  // the other slot early in the chunk), so the ticket's L2 round trip overlaps the chunk's
+  // first tile load instead of stalling the whole CTA between chunks.
+  if (t == 0) s_ticket[0] = atomicAdd(&a.nctr->sticket, 1u);
+  for (uint32_t ip = 0;; ++ip) {
     __syncthreads();
-    if (t == 0) s_ticket = atomicAdd(&a.nctr->sticket, 1u);
-    __syncthreads();
-    const uint32_t c = s_ticket;
+    const uint32_t c = s_ticket[ip & 1];
     if (c >= nchunk) break;
+    uint32_t* next_ticket = &s_ticket[(ip + 1) & 1];
     const ChunkDesc ch = a.chunks[c];
-    if (!a.seg_term[ch.seg]) continue;  // k_scatter_stable's chunk
+    if (!a.seg_term[ch.seg]) {  // k_scatter_stable's chunk
+      if (t == 0) *next_ticket = atomicAdd(&a.nctr->sticket, 1u);
+      continue;
+    }
     ModelDev md = a.models[ch.seg];
     tree_top_to_smem<TREE, kTThreads>(md, k);
     constexpr int kMain = TREE ? (int)kModelTree : (int)kModelLinear;
     if (md.kind == kModelEq3)
-      scatter_term_chunk<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw);
+      scatter_term_chunk<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw, next_ticket);
     else
-      scatter_term_chunk<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
+      scatter_term_chunk<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw, next_ticket);
     // this chunk's stores are visible before it counts; the last one reads them all
     __threadfence();
     __syncthreads();
     const SegDesc sg = a.segs[ch.seg];
-    if (t == 0) s_last = (atomicAdd(&a.seg_done[ch.seg], 1u) == sg.nchunks - 1) ? 1u : 0u;
-    __syncthreads();
-    if (!s_last) continue;
-    __threadfence();
+    if (sg.nchunks > 1) {  // block-uniform; a one-chunk segment is complete here
+      if (t == 0) s_last = (atomicAdd(&a.seg_done[ch.seg], 1u) == sg.nchunks - 1) ? 1u : 0u;
+      __syncthreads();
+      if (!s_last) continue;
+      __threadfence();
+    }
     // ---- the segment's windows (thread t owns child t) ----
     const uint32_t b = t;
     const uint32_t tot = (b < k) ? a.seg_tot[(size_t)ch.seg * k + b] : 0u;
@@ -2603,7 +2635,8 @@ __global__ __launch_bounds__(kTThreads, 1) void k_term_fused(LevelArgs a, uint64
     fence_proxy_async_smem();  // generic accesses (stage, scratch) before the warps' bulk loads
     __syncthreads();
     if (t == 0) atomicAdd((unsigned long long*)&a.nctr->term_keys, (unsigned long long)s_keys);
-    base_warp_windows<F64>(list, wp, s_nw, kWBWarps, dst_user, dst_scr, IN, bins, s_mbar[wp], it_base);
+    base_warp_windows<F64, true>(list, wp, s_nw, kWBWarps, dst_user, dst_scr, IN, bins, s_mbar[wp],
+                                 nullptr, it_base);
     fence_proxy_async_smem();  // and before the next chunk's tile ring
   }
 }
