@@ -40,6 +40,7 @@ KEY_U64 = 1
 MODEL_LINEAR = 0
 MODEL_EQ3 = 1
 MODEL_TREE = 2
+MODEL_TREE_EQ = 3   # sort option (R24): records carry kind MODEL_TREE
 DEFAULT_SEED = 0x49504C53  # "IPLS"
 
 
@@ -99,6 +100,7 @@ def lib():
         L.oracle_tree_splitters.argtypes = [vp, sz, u32, i32, vp]
         L.oracle_tree_splitters.restype = None
         L.oracle_tree_bucket.argtypes = [u64, i32, vp, u32]; L.oracle_tree_bucket.restype = u32
+        L.oracle_tree_eq_bucket.argtypes = [u64, i32, vp, u32]; L.oracle_tree_eq_bucket.restype = u32
         _lib = L
     return _lib
 
@@ -235,10 +237,20 @@ def tree_bucket(x, spl_ok: np.ndarray, k: int) -> int:
     return int(lib().oracle_tree_bucket(int(a.view(np.uint64)[0]), _key_type(a), _ptr(s), k))
 
 
+def tree_eq_bucket(x, spl_ok: np.ndarray, leaves: int) -> int:
+    """R24: bucket (of 2 * leaves) of one key under the tree with equality buckets."""
+    a = np.asarray([x])
+    if a.dtype not in (np.float64, np.uint64):
+        a = a.astype(np.float64)
+    s = np.ascontiguousarray(spl_ok, dtype=np.uint64)
+    return int(lib().oracle_tree_eq_bucket(int(a.view(np.uint64)[0]), _key_type(a), _ptr(s), leaves))
+
+
 def sort(keys: np.ndarray, k: int = 256, base_case: int = 4096, seed: int = DEFAULT_SEED,
          trace: bool = False, snapshots: bool = False, model: int = MODEL_LINEAR) -> SortResult:
     """Sort ``keys`` (float64 or uint64 numpy array) IN PLACE with the oracle; ``model``
-    MODEL_LINEAR (FMCD, IPLS) or MODEL_TREE (splitter tree, IPS4o's classifier)."""
+    MODEL_LINEAR (FMCD, IPLS), MODEL_TREE (splitter tree, IPS4o's classifier) or MODEL_TREE_EQ (the
+    tree with equality buckets, R24)."""
     if not keys.flags.c_contiguous:
         raise ValueError("keys must be C-contiguous")
     kt = _key_type(keys)

@@ -65,7 +65,8 @@ struct Model {
   uint32_t k;
   uint32_t D, capped;
   uint64_t pivot_ok;
-  const uint64_t* spl = nullptr;  /* TREE: k-1 sorted splitters (ordering keys) */
+  const uint64_t* spl = nullptr;  /* TREE: leaves-1 sorted splitters (ordering keys) */
+  uint32_t leaves = 0;            /* TREE: k, or k/2 with equality buckets (R24) */
 };
 
 /* R23: leaf of the descent j <- 2j + (x > a_j) = number of splitters strictly below x. */
@@ -73,9 +74,19 @@ uint32_t tree_bucket_of(uint64_t o, const uint64_t* spl, uint32_t k) {
   return (uint32_t)(std::lower_bound(spl, spl + (k - 1), o) - spl);
 }
 
+/* R24: leaf i of a tree of L leaves as above; the keys equal to splitter s_i take the
+ * equality bucket 2i+1, the keys strictly between s_{i-1} and s_i the bucket 2i. */
+uint32_t tree_eq_bucket_of(uint64_t o, const uint64_t* spl, uint32_t L) {
+  const uint32_t i = tree_bucket_of(o, spl, L);
+  const bool eq = i < L - 1 && spl[i] == o;
+  return 2 * i + (eq ? 1u : 0u);
+}
+
 /* P:394-402 with R7: y = RN(RN(A*v) + B); 0 if !(y >= 0); k-1 if y >= k; else floor(y). */
 uint32_t bucket_of(uint64_t bits, int key_type, const Model& md) {
-  if (md.kind == ORACLE_MODEL_TREE) return tree_bucket_of(ok_of(bits, key_type), md.spl, md.k);
+  if (md.kind == ORACLE_MODEL_TREE)
+    return md.leaves == md.k ? tree_bucket_of(ok_of(bits, key_type), md.spl, md.k)
+                             : tree_eq_bucket_of(ok_of(bits, key_type), md.spl, md.leaves);
   if (md.kind == ORACLE_MODEL_EQ3) {
     uint64_t o = ok_of(bits, key_type);
     if (o < md.pivot_ok) return 0;
@@ -184,6 +195,11 @@ uint32_t oracle_tree_bucket(uint64_t bits, int key_type, const uint64_t* spl_ok,
   return tree_bucket_of(ok_of(bits, key_type), spl_ok, k);
 }
 
+uint32_t oracle_tree_eq_bucket(uint64_t bits, int key_type, const uint64_t* spl_ok,
+                               uint32_t leaves) {
+  return tree_eq_bucket_of(ok_of(bits, key_type), spl_ok, leaves);
+}
+
 namespace {
 void partition_model(const uint64_t* in, uint64_t* out, size_t n, int key_type, const Model& md,
                      uint64_t* offsets, uint16_t* ids);
@@ -241,8 +257,10 @@ int oracle_sort(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32_t bas
 int oracle_sort_model(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32_t base_case,
                       uint64_t seed, int model, oracle_trace* trace) {
   if (k < 3 || k > 65535) return 1;
-  if (model != ORACLE_MODEL_LINEAR && model != ORACLE_MODEL_TREE) return 1;
+  if (model != ORACLE_MODEL_LINEAR && model != ORACLE_MODEL_TREE && model != ORACLE_MODEL_TREE_EQ)
+    return 1;
   if (model == ORACLE_MODEL_TREE && (k < 4 || (k & (k - 1)) != 0)) return 1;
+  if (model == ORACLE_MODEL_TREE_EQ && (k < 8 || (k & (k - 1)) != 0)) return 1;
   if (key_type != ORACLE_KEY_F64 && key_type != ORACLE_KEY_U64) return 1;
   if (n > 0 && keys == nullptr) return 1;
   /* Ingest: reject NaN before any write (R0). */
@@ -278,11 +296,14 @@ int oracle_sort_model(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32
       Model md{ORACLE_MODEL_LINEAR, 0.0, 0.0, k, 0, 0, 0};
       std::vector<uint64_t> spl;
       bool eq3 = sg.force_eq3 || S < 4;
-      if (!eq3 && model == ORACLE_MODEL_TREE) {
-        spl.resize(k - 1);
-        oracle_tree_splitters(smp.data(), S, k, key_type, spl.data());
+      if (!eq3 && (model == ORACLE_MODEL_TREE || model == ORACLE_MODEL_TREE_EQ)) {
+        /* R24: with equality buckets the k buckets are k/2 leaves x {between, equal}. */
+        const uint32_t leaves = model == ORACLE_MODEL_TREE_EQ ? k / 2 : k;
+        spl.resize(leaves - 1);
+        oracle_tree_splitters(smp.data(), S, leaves, key_type, spl.data());
         md.kind = ORACLE_MODEL_TREE;
         md.spl = spl.data();
+        md.leaves = leaves;
       } else if (!eq3) {
         std::vector<double> sv(S);
         for (uint64_t j = 0; j < S; ++j) sv[j] = value_of(smp[j], key_type);

@@ -23,7 +23,8 @@ extern "C" {
 #endif
 
 enum { ORACLE_KEY_F64 = 0, ORACLE_KEY_U64 = 1 };
-enum { ORACLE_MODEL_LINEAR = 0, ORACLE_MODEL_EQ3 = 1, ORACLE_MODEL_TREE = 2 };
+enum { ORACLE_MODEL_LINEAR = 0, ORACLE_MODEL_EQ3 = 1, ORACLE_MODEL_TREE = 2,
+       ORACLE_MODEL_TREE_EQ = 3 /* a sort option: its records carry kind ORACLE_MODEL_TREE */ };
 
 /* Order-preserving key ("extractor ... maps double to integers"). */
 uint64_t oracle_ordering_key(uint64_t bits, int key_type);
@@ -64,6 +65,12 @@ void oracle_tree_splitters(const uint64_t* sorted_bits, size_t S, uint32_t k, in
  * implicit tree of the splitters ends at leaf #{i : spl_i < ok(x)} (ties go left, R23),
  * which is what this returns (the plain definition, by binary search). */
 uint32_t oracle_tree_bucket(uint64_t bits, int key_type, const uint64_t* spl_ok, uint32_t k);
+/* IPS4o's equality buckets ("a bucket B_i just for the elements x = s_i"; DESIGN.md
+ * R24): a tree of `leaves` leaves (leaves-1 splitters spl_ok) feeds 2*leaves buckets; a key in
+ * leaf i goes to bucket 2i+1 if it equals splitter s_i (i < leaves-1), else to bucket 2i.
+ * Every odd bucket holds one value, so it is final after the partition. */
+uint32_t oracle_tree_eq_bucket(uint64_t bits, int key_type, const uint64_t* spl_ok,
+                               uint32_t leaves);
 
 /* One record per partitioned segment, in level order then increasing begin. */
 typedef struct {
@@ -95,7 +102,9 @@ const uint64_t* oracle_trace_snapshot(const oracle_trace* t, uint32_t level);
 int oracle_sort(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32_t base_case,
                 uint64_t seed, oracle_trace* trace);
 /* Same with the model chosen: ORACLE_MODEL_LINEAR (FMCD, the paper's IPLS) or
- * ORACLE_MODEL_TREE (splitter tree, IPS4o's classifier; k must be a power of two >= 4). */
+ * ORACLE_MODEL_TREE (splitter tree, IPS4o's classifier; k must be a power of two >= 4) or
+ * ORACLE_MODEL_TREE_EQ (the tree with equality buckets, R24: k/2 leaves, k buckets; k a
+ * power of two >= 8). */
 int oracle_sort_model(uint64_t* keys, size_t n, int key_type, uint32_t k, uint32_t base_case,
                       uint64_t seed, int model, oracle_trace* trace);
 
