@@ -51,6 +51,12 @@ typedef enum { IPLS_MODEL_LINEAR = 0, IPLS_MODEL_EQ3 = 1, IPLS_MODEL_TREE = 2 } 
  * descends j <- 2j + (x > a_j) (ties left).  k must be a power of two.  Degenerate cases
  * and the no-progress guard are the same (EQ3).  Trace records carry kind IPLS_MODEL_TREE. */
 #define IPLS_FLAG_TREE_MODEL 1u
+/* IPLS_FLAG_TREE_EQUAL_BUCKETS (only with IPLS_FLAG_TREE_MODEL; k a power of two >= 8):
+ * IPS4o's equality buckets ("a bucket B_i just for the elements x = s_i"; DESIGN.md
+ * R24).  The tree has k / 2 leaves (k / 2 - 1 splitters s_0 <= s_1 <= ...); a key in leaf i
+ * goes to bucket 2i + 1 if it equals s_i and to bucket 2i otherwise, so the k buckets stay
+ * range-ordered and every odd bucket holds one value (final after the partition). */
+#define IPLS_FLAG_TREE_EQUAL_BUCKETS 2u
 
 #define IPLS_MAX_K 1024u          /* fan-out limit of the sm_100a kernels (smem-resident) */
 #define IPLS_MAX_BASE_CASE 4096u  /* base-case limit (n <= 2^12)                    */
@@ -60,7 +66,8 @@ typedef struct {
   uint32_t k;         /* buckets per level, 3..IPLS_MAX_K (P:473 uses 256)                 */
   uint32_t base_case; /* segments of <= base_case keys go to the base case, 1..4096 */
   uint64_t seed;      /* sampling seed (R18)                                               */
-  uint32_t flags;     /* 0 or IPLS_FLAG_TREE_MODEL (k a power of two); other bits: invalid  */
+  uint32_t flags;     /* 0, IPLS_FLAG_TREE_MODEL (k a power of two), or that with
+                         IPLS_FLAG_TREE_EQUAL_BUCKETS; other bits or combinations: invalid  */
 } ipls_config;
 
 typedef struct {

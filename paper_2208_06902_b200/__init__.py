@@ -29,7 +29,10 @@ KEY_U64 = 1
 MODEL_LINEAR = 0
 MODEL_EQ3 = 1
 MODEL_TREE = 2        # splitter tree (IPS4o's classifier; config flag FLAG_TREE_MODEL)
+MODEL_TREE_EQ = 3     # sort option: the tree with IPS4o's equality buckets (R24);
+                      # trace records carry kind MODEL_TREE
 FLAG_TREE_MODEL = 1
+FLAG_TREE_EQUAL_BUCKETS = 2
 DEFAULT_SEED = 0x49504C53
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "NaN key", 3: "degenerate sample",
@@ -153,10 +156,13 @@ def _check(st: int):
 
 
 def _cfg(k: int, base_case: int, seed: int, model: int = MODEL_LINEAR) -> _Config:
-    """model: MODEL_LINEAR (FMCD, the paper's IPLS) or MODEL_TREE (splitter tree)."""
-    if model not in (MODEL_LINEAR, MODEL_TREE):
-        raise ValueError("model must be MODEL_LINEAR or MODEL_TREE")
-    return _Config(k, base_case, seed, FLAG_TREE_MODEL if model == MODEL_TREE else 0)
+    """model: MODEL_LINEAR (FMCD, the paper's IPLS), MODEL_TREE (splitter tree) or MODEL_TREE_EQ
+    (the tree with equality buckets)."""
+    if model not in (MODEL_LINEAR, MODEL_TREE, MODEL_TREE_EQ):
+        raise ValueError("model must be MODEL_LINEAR, MODEL_TREE or MODEL_TREE_EQ")
+    flags = {MODEL_TREE: FLAG_TREE_MODEL,
+             MODEL_TREE_EQ: FLAG_TREE_MODEL | FLAG_TREE_EQUAL_BUCKETS}.get(model, 0)
+    return _Config(k, base_case, seed, flags)
 
 
 def _stream(stream) -> Optional[int]:

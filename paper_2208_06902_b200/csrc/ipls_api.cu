@@ -121,6 +121,7 @@ struct Params {
   uint32_t k, B, chunk_keys;
   uint32_t cap_segs, cap_chunks, cap_samples, cap_wins, cap_wbig, cap_fills, cap_twin;
   bool tree;  // IPLS_FLAG_TREE_MODEL: splitter-tree model instead of FMCD
+  uint32_t tree_leaves;  // tree: k, or k / 2 with IPLS_FLAG_TREE_EQUAL_BUCKETS (R24)
 };
 
 #ifndef IPLS_CHUNK_CAP
@@ -138,9 +139,10 @@ uint32_t pick_chunk_keys(uint64_t n) {
   return (uint32_t)c;
 }
 
-Params make_params(uint64_t n, uint32_t k, uint32_t B, bool tree = false) {
+Params make_params(uint64_t n, uint32_t k, uint32_t B, bool tree = false, bool tree_eq = false) {
   Params p{};
   p.n = n; p.k = k; p.B = B; p.tree = tree;
+  p.tree_leaves = tree ? (tree_eq ? k / 2 : k) : 0;
   p.chunk_keys = pick_chunk_keys(n);
   const uint64_t segs = n / ((uint64_t)B + 1) + 2;
   const uint64_t chunks = n / p.chunk_keys + segs + 1;
@@ -619,17 +621,20 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
       uint32_t* redo_cnt = &cctr->n_redo;                 // zero: cleared with the counters
       if (max_S <= (uint32_t)kFMMax)
         k_fit_small<F64, kFSThreads, kFMItems><<<nseg, kFSThreads, kFMSmem, st>>>(
-            src, segs, seed, hbase, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
+            src, segs, seed, hbase, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt,
+            p.tree_leaves);
       else if (max_S <= (uint32_t)kFSMax)
         k_fit_small<F64, kFSThreads, kFSItems><<<nseg, kFSThreads, kFSSmem, st>>>(
-            src, segs, seed, hbase, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
+            src, segs, seed, hbase, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt,
+            p.tree_leaves);
       else
         k_fit_small<F64, kFLThreads, kFLItems><<<nseg, kFLThreads, kFLSmem, st>>>(
-            src, segs, seed, hbase, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt);
+            src, segs, seed, hbase, level, k, trace ? samples : nullptr, models, redo, tree, redo_cnt,
+            p.tree_leaves);
       ck_launch();
       k_gather_fit<F64><<<std::min(nseg, num_sms()), kFitThreads, fit_smem(cap), st>>>(
           src, segs, seed, hbase, level, k, cap, trace ? samples : nullptr, models, nullptr, redo, tree, 0,
-          redo_cnt);
+          redo_cnt, p.tree_leaves);
       ck_launch();
     }
     LevelArgs la{};
@@ -784,9 +789,11 @@ ipls_status check_cfg(const ipls_config* cfg, ipls_config* out) {
   ipls_config c = cfg ? *cfg : ipls_default_config();
   if (c.k < 3 || c.k > IPLS_MAX_K) return IPLS_ERR_INVALID_ARGUMENT;
   if (c.base_case < 1 || c.base_case > IPLS_MAX_BASE_CASE) return IPLS_ERR_INVALID_ARGUMENT;
-  if (c.flags & ~IPLS_FLAG_TREE_MODEL) return IPLS_ERR_INVALID_ARGUMENT;
+  if (c.flags & ~(IPLS_FLAG_TREE_MODEL | IPLS_FLAG_TREE_EQUAL_BUCKETS)) return IPLS_ERR_INVALID_ARGUMENT;
   if ((c.flags & IPLS_FLAG_TREE_MODEL) && (c.k < 4 || (c.k & (c.k - 1)) != 0))
     return IPLS_ERR_INVALID_ARGUMENT;  // the splitter tree is a perfect binary tree
+  if (c.flags & IPLS_FLAG_TREE_EQUAL_BUCKETS)  // k / 2 leaves, each with its equality bucket
+    if (!(c.flags & IPLS_FLAG_TREE_MODEL) || c.k < 8) return IPLS_ERR_INVALID_ARGUMENT;
   *out = c;
   return IPLS_OK;
 }
@@ -804,7 +811,8 @@ ipls_status sort_impl(void* d_keys, size_t n, ipls_key_type t, const ipls_config
   if (n <= 1) return IPLS_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   try {
-    const Params p = make_params(n, cfg.k, cfg.base_case, (cfg.flags & IPLS_FLAG_TREE_MODEL) != 0);
+    const Params p = make_params(n, cfg.k, cfg.base_case, (cfg.flags & IPLS_FLAG_TREE_MODEL) != 0,
+                                  (cfg.flags & IPLS_FLAG_TREE_EQUAL_BUCKETS) != 0);
     const FixedLayout FL = fixed_layout(p);
     StreamCache& sc = cache_for(stream);
     void* fixed;
@@ -970,7 +978,8 @@ size_t ipls_workspace_bytes(size_t n, ipls_key_type t, const ipls_config* cfg) {
   ipls_config c;
   if (check_cfg(cfg, &c) != IPLS_OK || (t != IPLS_KEY_F64 && t != IPLS_KEY_U64)) return 0;
   if (n <= 1) return 0;
-  const Params p = make_params(n, c.k, c.base_case, (c.flags & IPLS_FLAG_TREE_MODEL) != 0);
+  const Params p = make_params(n, c.k, c.base_case, (c.flags & IPLS_FLAG_TREE_MODEL) != 0,
+                                (c.flags & IPLS_FLAG_TREE_EQUAL_BUCKETS) != 0);
   return fixed_layout(p).total + worst_meta_bytes(p);
 }
 

@@ -33,7 +33,8 @@ struct ModelDev {           // fitted model of one segment (Listing 1 outputs, E
   double A, B;
   uint64_t pivot_ok;
   uint32_t kind, D, capped, k_eff;
-  const uint64_t* heap;     // tree: splitters (ordering keys) in heap order, heap[1..k-1]
+  uint32_t leaves, pad_;    // tree: leaves of the splitter tree (k, or k / 2 with equality buckets)
+  const uint64_t* heap;     // tree: splitters (ordering keys) in heap order, heap[1..leaves-1]
   const uint64_t* top;      // tree, set per CTA: smem copy of heap[0..256) (the top 8 levels)
 };
 
@@ -102,7 +103,9 @@ __device__ __forceinline__ uint32_t linear_bucket(double v, double A, double B, 
 // at compile time (the kind is uniform per chunk).  Tree: the branchless descent
 // j <- 2j + (x > a_j) of P:377-379 over the implicit tree of the k-1 splitters (k a power of
 // two); the top 8 levels come from the CTA's smem copy, deeper levels through the L1; ties go
-// left (R23).
+// left (R23).  Equality buckets (R24: a tree of k / 2 leaves): the splitter of the node
+// where the descent last went left is the least splitter >= x, i.e. the leaf's own splitter
+// s_i; a key equal to it takes bucket 2i + 1, any other key of leaf i bucket 2i.
 template <bool F64, int MODE>
 struct Bucketer {
   double A, B;
@@ -111,10 +114,16 @@ struct Bucketer {
   const uint64_t* heap;
   const uint64_t* top;
   int depth;
+  uint32_t leaves;
+  bool eqb;
   __device__ __forceinline__ explicit Bucketer(const ModelDev& md, uint32_t k)
-      : A(md.A), B(md.B), piv(md.pivot_ok), km1(k - 1), heap(md.heap), top(md.top), depth(0) {
-    if constexpr (MODE == (int)kModelTree)
-      while ((2u << depth) <= k) ++depth;  // log2 k (k a power of two)
+      : A(md.A), B(md.B), piv(md.pivot_ok), km1(k - 1), heap(md.heap), top(md.top), depth(0),
+        leaves(k), eqb(false) {
+    if constexpr (MODE == (int)kModelTree) {
+      leaves = md.leaves;
+      eqb = md.leaves != k;
+      while ((2u << depth) <= leaves) ++depth;  // log2 leaves (a power of two)
+    }
   }
   __device__ __forceinline__ uint32_t operator()(uint64_t bits) const {
     if constexpr (MODE == (int)kModelEq3) {
@@ -124,9 +133,25 @@ struct Bucketer {
       const uint64_t o = ok_of<F64>(bits);
       uint32_t j = 1;
       const int dt = depth < 8 ? depth : 8;
-      for (int d = 0; d < dt; ++d) j = 2 * j + (o > top[j] ? 1u : 0u);
-      for (int d = dt; d < depth; ++d) j = 2 * j + (o > __ldg(heap + j) ? 1u : 0u);
-      return j - (km1 + 1);
+      if (!eqb) {
+        for (int d = 0; d < dt; ++d) j = 2 * j + (o > top[j] ? 1u : 0u);
+        for (int d = dt; d < depth; ++d) j = 2 * j + (o > __ldg(heap + j) ? 1u : 0u);
+        return j - leaves;
+      }
+      uint64_t last = ~o;  // splitter of the last left turn; != o while there was none
+      for (int d = 0; d < dt; ++d) {
+        const uint64_t s = top[j];
+        const bool right = o > s;
+        last = right ? last : s;
+        j = 2 * j + (right ? 1u : 0u);
+      }
+      for (int d = dt; d < depth; ++d) {
+        const uint64_t s = __ldg(heap + j);
+        const bool right = o > s;
+        last = right ? last : s;
+        j = 2 * j + (right ? 1u : 0u);
+      }
+      return 2 * (j - leaves) + (o == last ? 1u : 0u);
     } else {
       return linear_bucket(value_of<F64>(bits), A, B, km1);
     }

@@ -263,7 +263,7 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
     uint64_t hbase, uint32_t level, uint32_t k, uint32_t cap, uint64_t* __restrict__ samples_out,
     ModelDev* __restrict__ models, const uint64_t* __restrict__ presorted_ok,
     const uint32_t* __restrict__ redo, uint64_t* __restrict__ tree, int sort_given = 0,
-    const uint32_t* __restrict__ redo_cnt = nullptr) {
+    const uint32_t* __restrict__ redo_cnt = nullptr, uint32_t tree_leaves = 0) {
   // With redo_cnt: the CTAs walk the list redo[0, *redo_cnt) of segments k_fit_small left over
   // (usually none: a launch of a few idle CTAs).  Without: CTA s fits segment s.
   const uint32_t nitems = redo_cnt ? *((volatile const uint32_t*)redo_cnt) : 1u;
@@ -320,8 +320,9 @@ __global__ __launch_bounds__(kFitThreads) void k_gather_fit(
   bool eq3 = (sg.flags & kSegForceEq3) || S < 4;
   if (!eq3 && tree) {  // splitter-tree model instead of FMCD
     uint64_t* hp = tree + (size_t)sgi * kMaxK;
-    write_tree<kFitThreads>(a, S, k, hp);
-    md.kind = kModelTree; md.heap = hp;
+    const uint32_t leaves = tree_leaves ? tree_leaves : k;  // k / 2 with equality buckets (R24)
+    write_tree<kFitThreads>(a, S, leaves, hp);
+    md.kind = kModelTree; md.heap = hp; md.leaves = leaves;
   } else if (!eq3) {
     double* s = reinterpret_cast<double*>(tmp);
     for (uint32_t i = threadIdx.x; i < S; i += kFitThreads) s[i] = value_of<F64>(bits_of_ok<F64>(a[i]));
@@ -400,7 +401,8 @@ __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
     const uint64_t* __restrict__ src, const SegDesc* __restrict__ segs, uint64_t seed,
     uint64_t hbase, uint32_t level, uint32_t k, uint64_t* __restrict__ samples_out,
     ModelDev* __restrict__ models,
-    uint32_t* __restrict__ redo, uint64_t* __restrict__ tree, uint32_t* __restrict__ redo_cnt) {
+    uint32_t* __restrict__ redo, uint64_t* __restrict__ tree, uint32_t* __restrict__ redo_cnt,
+    uint32_t tree_leaves) {
   constexpr int NW = NT / 32, SMAX = NT * IT;
   static_assert(NT >= 256 && IT % 4 == 0, "256 coarse bins, uint4 fine-bin scan");
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -637,8 +639,9 @@ __global__ __launch_bounds__(NT, NT == 256 ? 3 : 1) void k_fit_small(
   bool eq3 = (sg.flags & kSegForceEq3) || S < 4;
   if (!eq3 && tree) {  // splitter-tree model instead of FMCD
     uint64_t* hp = tree + (size_t)blockIdx.x * kMaxK;
-    write_tree<NT>(B, S, k, hp);
-    md.kind = kModelTree; md.heap = hp;
+    const uint32_t leaves = tree_leaves ? tree_leaves : k;  // k / 2 with equality buckets (R24)
+    write_tree<NT>(B, S, leaves, hp);
+    md.kind = kModelTree; md.heap = hp; md.leaves = leaves;
   } else if (!eq3) {
     double* s = reinterpret_cast<double*>(B);
     for (uint32_t i = threadIdx.x; i < S; i += NT) s[i] = value_of<F64>(bits_of_ok<F64>(B[i]));

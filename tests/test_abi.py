@@ -58,6 +58,12 @@ def test_host_only_calls(native):
     assert native.ipls_sort_f64(None, 0, None) == 0
     bad = ipls._Config(2, 4096, 1, 0)
     assert native.ipls_sort_ex(None, 0, 0, ctypes.byref(bad), None, 0, None) == 1
+    # flags: equality buckets only with the tree model, k a power of two >= 8 (R24)
+    for k, flags, ok in [(1024, 1, True), (1024, 3, True), (8, 3, True), (4, 3, False),
+                         (1024, 2, False), (1000, 3, False), (1024, 4, False)]:
+        c = ipls._Config(k, 4096, 1, flags)
+        assert (native.ipls_sort_ex(None, 0, 0, ctypes.byref(c), None, 0, None) == 0) == ok
+        assert (native.ipls_workspace_bytes(10 ** 6, 0, ctypes.byref(c)) > 0) == ok
 
 
 def test_no_oracle_in_product_path():

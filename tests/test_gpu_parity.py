@@ -275,6 +275,68 @@ def test_tree_model_configs_scaled(ipls, name):
     compare_traces(gtr, ores)
 
 
+@pytest.mark.parametrize("kind", TREE_KINDS)
+@pytest.mark.parametrize("n,k,B", [(5000, 16, 64), (70_001, 256, 4096), (300_000, 1024, 4096)])
+def test_tree_equal_buckets_parity(ipls, kind, n, k, B):
+    """The tree with IPS4o's equality buckets (R24): samples, per-segment counts, every
+    level's layout and the final array, bit-exact against the oracle's MODEL_TREE_EQ."""
+    rng = np.random.default_rng(n + k + len(kind) + 1)
+    a = datagen.fuzz_array(rng, n, kind)
+    want = a.copy()
+    ores = oracle.sort(want, k=k, base_case=B, trace=True, snapshots=True,
+                       model=oracle.MODEL_TREE_EQ)
+    t = dev(a)
+    gtr = ipls.sort_trace(t, k=k, base_case=B, key_type=kt_of(a),
+                          snapshot_levels=max(1, ores.levels), model=ipls.MODEL_TREE_EQ)
+    assert host(t, a.dtype).tobytes() == want.tobytes()
+    compare_traces(gtr, ores)
+    # the untraced entry point gives the same bytes
+    t2 = dev(a)
+    ipls.sort(t2, k=k, base_case=B, key_type=kt_of(a), model=ipls.MODEL_TREE_EQ)
+    assert torch.equal(t, t2)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_tree_equal_buckets_configs_scaled(ipls, name):
+    a = datagen.generate(name, 2_000_000)
+    cfg = datagen.CONFIGS[name]
+    want = a.copy()
+    ores = oracle.sort(want, k=cfg.k, base_case=cfg.base_case, trace=True,
+                       model=oracle.MODEL_TREE_EQ)
+    t = dev(a)
+    gtr = ipls.sort_trace(t, k=cfg.k, base_case=cfg.base_case, key_type=kt_of(a),
+                          model=ipls.MODEL_TREE_EQ)
+    assert host(t, a.dtype).tobytes() == want.tobytes()
+    compare_traces(gtr, ores)
+
+
+def test_tree_equal_buckets_heavy_duplicates(ipls):
+    """Half of the keys share one value (P:382's case): all of them are final after level 0,
+    exactly as in the oracle."""
+    rng = np.random.default_rng(7)
+    n = 1_000_000
+    a = rng.random(n)
+    a[rng.random(n) < 0.5] = 0.5
+    want = a.copy()
+    ores = oracle.sort(want, k=1024, base_case=4096, trace=True, snapshots=True,
+                       model=oracle.MODEL_TREE_EQ)
+    t = dev(a)
+    gtr = ipls.sort_trace(t, k=1024, base_case=4096, key_type=kt_of(a),
+                          snapshot_levels=max(1, ores.levels), model=ipls.MODEL_TREE_EQ)
+    assert host(t, a.dtype).tobytes() == want.tobytes()
+    compare_traces(gtr, ores)
+    assert sum(r.m for r in gtr.records if r.level >= 1) <= n - int((a == 0.5).sum())
+
+
+def test_tree_equal_buckets_flag_validation(ipls):
+    t = dev(np.random.default_rng(0).random(10000))
+    with pytest.raises(ipls.IPLSError):
+        ipls.sort(t, k=4, model=ipls.MODEL_TREE_EQ)       # k >= 8
+    with pytest.raises(ipls.IPLSError):
+        ipls.sort(t, k=1000, model=ipls.MODEL_TREE_EQ)    # k a power of two
+    assert ipls.workspace_bytes(10000, ipls.KEY_F64, k=4, model=ipls.MODEL_TREE_EQ) == 0
+
+
 def test_tree_model_nan_rejected_unmodified(ipls):
     a = np.random.default_rng(3).normal(0, 1, 300_000)
     a[123_456] = np.nan
