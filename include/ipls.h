@@ -156,6 +156,32 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
  * its G runs into bucket-major order (ipls_regroup_runs) and resumes the recursion at level 1
  * (ipls_sort_segments).  Rank r then holds the r-th key range. */
 
+/* The exchange fused into the partition (DESIGN.md §7 "fused exchange"; every
+ * thread -- here every GPU -- moves its keys straight into the buckets' final places).
+ * Instead of steps (3) and (5)'s partition + all-to-all + regroup, a rank (3') counts its
+ * buckets (ipls_partition_count), the counts are all-gathered and the plan of step (4) gives,
+ * for every bucket b, the address in the owning rank's receive buffer where this rank's keys
+ * of b belong (bucket-major, then source rank: base of b in the owner's buffer + the counts of
+ * b on lower ranks), and (5') ipls_partition_scatter_to writes them there directly (peer
+ * memory over NVLink; plain 8-byte stores in runs of consecutive keys).  After a barrier the
+ * owner's buffer is what ipls_regroup_runs would have produced.
+ *
+ * ipls_partition_count: the classify half of ipls_partition_level.  d_in: n keys (device);
+ * d_offsets: k_eff+1 uint64 bucket boundaries of the stable partition (device).
+ * ipls_partition_scatter_to: classifies again (the per-chunk prefixes are not kept between
+ * calls: 8 B/key of reads buy a stateless interface) and scatters stably: this array's keys
+ * of bucket b, in input order, go to the consecutive 64-bit words starting at the ADDRESS
+ * d_bucket_dst[b] (device array of k_eff addresses, each 8-byte aligned, of memory the
+ * device can store to: its own or a peer's mapped allocation); the destinations of different
+ * buckets must not overlap each other or d_in.  Entries of empty buckets are ignored.
+ * Both: models LINEAR or EQ3, n <= 2^32-1, synchronise `stream`; errors as
+ * ipls_partition_level. */
+ipls_status ipls_partition_count(const void* d_in, size_t n, ipls_key_type t,
+                                 const ipls_model* h_model, uint64_t* d_offsets, void* stream);
+ipls_status ipls_partition_scatter_to(const void* d_in, size_t n, ipls_key_type t,
+                                      const ipls_model* h_model, const uint64_t* d_bucket_dst,
+                                      void* stream);
+
 /* Sort n keys that form nseg consecutive range-ordered segments -- every key of segment i
  * precedes (ordering key) every key of segment i+1 -- by resuming the recursion
  * at `level`: each segment of more than base_case keys is partitioned as a

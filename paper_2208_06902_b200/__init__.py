@@ -88,7 +88,8 @@ SYMBOLS = ["ipls_default_config", "ipls_sort_f64", "ipls_sort_u64", "ipls_sort_e
            "ipls_kernel_launch_count", "ipls_profile_enable", "ipls_profile_reset",
            "ipls_profile_read", "ipls_sample_size", "ipls_sample_strata", "ipls_assign_ranges", "ipls_assign_cuts", "ipls_fit_sample", "ipls_debug_set_epoch",
            "ipls_debug_force_match_rank", "ipls_sort_segments",
-           "ipls_regroup_runs", "ipls_sort_segments_trace", "ipls_debug_term_mode"]
+           "ipls_regroup_runs", "ipls_sort_segments_trace", "ipls_debug_term_mode",
+           "ipls_partition_count", "ipls_partition_scatter_to"]
 
 _lib = None
 
@@ -117,6 +118,10 @@ def lib():
         L.ipls_fit_fmcd.restype = i32
         L.ipls_partition_level.argtypes = [vp, vp, sz, i32, ctypes.POINTER(_Model), vp, vp, vp]
         L.ipls_partition_level.restype = i32
+        L.ipls_partition_count.argtypes = [vp, sz, i32, ctypes.POINTER(_Model), vp, vp]
+        L.ipls_partition_count.restype = i32
+        L.ipls_partition_scatter_to.argtypes = [vp, sz, i32, ctypes.POINTER(_Model), vp, vp]
+        L.ipls_partition_scatter_to.restype = i32
         L.ipls_sort_trace.argtypes = [vp, sz, i32, ctypes.POINTER(_Config), ctypes.POINTER(_Trace), vp]
         L.ipls_sort_trace.restype = i32
         L.ipls_status_string.argtypes = [i32]; L.ipls_status_string.restype = ctypes.c_char_p
@@ -329,6 +334,37 @@ def partition_level(keys_in, keys_out, model: Model, key_type: Optional[int] = N
                                       ids.data_ptr() if ids is not None else None,
                                       _stream(stream)))
     return off, (ids[:keys_in.numel()] if ids is not None else None)
+
+
+def partition_count(keys_in, model: Model, key_type: Optional[int] = None, stream=None):
+    """The classify half of partition_level: the k_eff + 1 bucket boundaries of keys_in's stable
+    partition (int64 CUDA tensor).  include/ipls.h: ipls_partition_count."""
+    import torch
+    _check_tensor(keys_in)
+    kt = _key_type_of(keys_in, key_type)
+    ke = 3 if model.kind == MODEL_EQ3 else model.k
+    off = torch.empty(ke + 1, dtype=torch.int64, device=keys_in.device)
+    m = _Model(model.a, model.b, model.k, model.D, model.kind, model.capped, model.pivot_ok)
+    _check(lib().ipls_partition_count(keys_in.data_ptr(), keys_in.numel(), kt, ctypes.byref(m),
+                                      off.data_ptr(), _stream(stream)))
+    return off
+
+
+def partition_scatter_to(keys_in, model: Model, bucket_dst, key_type: Optional[int] = None,
+                         stream=None) -> None:
+    """Stable scatter of keys_in with one destination per bucket: bucket b's keys go to the
+    64-bit words from ADDRESS bucket_dst[b] on (int64 CUDA tensor of k_eff device addresses:
+    own or peer memory).  include/ipls.h: ipls_partition_scatter_to."""
+    _check_tensor(keys_in)
+    _check_tensor(bucket_dst)
+    kt = _key_type_of(keys_in, key_type)
+    ke = 3 if model.kind == MODEL_EQ3 else model.k
+    if bucket_dst.numel() < ke:
+        raise ValueError("bucket_dst must hold one address per bucket")
+    m = _Model(model.a, model.b, model.k, model.D, model.kind, model.capped, model.pivot_ok)
+    _check(lib().ipls_partition_scatter_to(keys_in.data_ptr(), keys_in.numel(), kt,
+                                           ctypes.byref(m), bucket_dst.data_ptr(),
+                                           _stream(stream)))
 
 
 def sample_size(m: int, k: int) -> int:

@@ -380,6 +380,8 @@ void set_attrs() {
                           (int)base_smem()));
   ck(cudaFuncSetAttribute(k_base_warp<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)warp_base_smem()));
+  ck(cudaFuncSetAttribute(k_scatter_peer<F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)scatter_peer_smem_bytes(kMaxK)));
   for (int tr = 0; tr < 2; ++tr) {
     ck(cudaFuncSetAttribute(tr ? k_classify_scan<F64, true> : k_classify_scan<F64, false>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)classify_smem(kMaxK)));
@@ -1221,11 +1223,22 @@ ipls_status ipls_assign_cuts(const uint64_t* h_counts, uint32_t k, uint32_t G,
   return IPLS_OK;
 }
 
-ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_key_type t,
-                                 const ipls_model* h_model, uint64_t* d_offsets,
-                                 uint16_t* d_bucket_ids, void* stream) {
-  if (!h_model || !d_offsets) return IPLS_ERR_INVALID_ARGUMENT;
-  if (n > 0 && (!d_in || !d_out)) return IPLS_ERR_INVALID_ARGUMENT;
+}  // extern "C"
+
+namespace {
+// ipls_partition_level and its two halves for the fused multi-GPU exchange: kPartCount
+// classifies only (offsets), kPartScatterTo classifies and scatters every bucket to its own
+// destination address (k_scatter_peer).
+enum PartMode { kPartFull, kPartCount, kPartScatterTo };
+
+ipls_status partition_impl(PartMode mode, const void* d_in, void* d_out, size_t n, ipls_key_type t,
+                           const ipls_model* h_model, uint64_t* d_offsets,
+                           uint16_t* d_bucket_ids, const uint64_t* d_bucket_dst, void* stream) {
+  if (!h_model) return IPLS_ERR_INVALID_ARGUMENT;
+  if (mode != kPartScatterTo && !d_offsets) return IPLS_ERR_INVALID_ARGUMENT;
+  if (n > 0 && !d_in) return IPLS_ERR_INVALID_ARGUMENT;
+  if (n > 0 && mode == kPartFull && !d_out) return IPLS_ERR_INVALID_ARGUMENT;
+  if (n > 0 && mode == kPartScatterTo && !d_bucket_dst) return IPLS_ERR_INVALID_ARGUMENT;
   if (n > 0xFFFFFFFFull) return IPLS_ERR_INVALID_ARGUMENT;
   if (t != IPLS_KEY_F64 && t != IPLS_KEY_U64) return IPLS_ERR_INVALID_ARGUMENT;
   const bool eq3 = h_model->kind == IPLS_MODEL_EQ3;
@@ -1235,9 +1248,11 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   try {
     if (n == 0) {
-      std::vector<uint64_t> z(k + 1, 0);
-      ck(cudaMemcpyAsync(d_offsets, z.data(), z.size() * 8, cudaMemcpyHostToDevice, st));
-      ck(cudaStreamSynchronize(st));
+      if (d_offsets) {
+        std::vector<uint64_t> z(k + 1, 0);
+        ck(cudaMemcpyAsync(d_offsets, z.data(), z.size() * 8, cudaMemcpyHostToDevice, st));
+        ck(cudaStreamSynchronize(st));
+      }
       return IPLS_OK;
     }
     StreamCache& sc = cache_for(stream);
@@ -1245,6 +1260,7 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
     const uint32_t nchunk = (uint32_t)((n + ck_keys - 1) / ck_keys);
     const MetaLayout ML = meta_layout(1, nchunk, 0, k);
     size_t o = align_up(ML.total, 256);
+    const size_t off_own = o; o = align_up(o + (size_t)(k + 1) * 8, 256);  // offsets nobody asked for
     const size_t off_seg = o; o += 256;
     const size_t off_ch = o; o = align_up(o + nchunk * sizeof(ChunkDesc), 256);
     const size_t off_err = o; o += 256;
@@ -1284,13 +1300,20 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
     la.err = derr;
     la.check_nan = 0;
     la.ids = d_bucket_ids;
-    la.single_offsets = d_offsets;
+    la.single_offsets = d_offsets ? d_offsets : at<uint64_t>(meta, off_own);
+    la.bucket_dst = d_bucket_dst;
     uint64_t* out = static_cast<uint64_t*>(d_out);
     auto body = [&](auto f64tag) {
       constexpr bool F64 = decltype(f64tag)::value;
       set_attrs<F64>();
       launch_classify<F64>(nchunk, st, la);
-      launch_scatter<F64>(nchunk, st, la, out, out, false, true);
+      if (mode == kPartFull) {
+        launch_scatter<F64>(nchunk, st, la, out, out, false, true);
+      } else if (mode == kPartScatterTo) {
+        IPLS_PROF("scatter_peer", 16.0 * n);
+        k_scatter_peer<F64><<<nchunk, kSThreads, scatter_peer_smem_bytes(k), st>>>(la);
+        ck_launch();
+      }
     };
     if (t == IPLS_KEY_F64) body(std::true_type{}); else body(std::false_type{});
     ck(cudaStreamSynchronize(st));
@@ -1299,6 +1322,29 @@ ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_k
     g_last_cuda_error = cudaGetErrorString(f.e);
     return IPLS_ERR_CUDA;
   }
+}
+}  // namespace
+
+extern "C" {
+
+ipls_status ipls_partition_level(const void* d_in, void* d_out, size_t n, ipls_key_type t,
+                                 const ipls_model* h_model, uint64_t* d_offsets,
+                                 uint16_t* d_bucket_ids, void* stream) {
+  return partition_impl(kPartFull, d_in, d_out, n, t, h_model, d_offsets, d_bucket_ids, nullptr,
+                        stream);
+}
+
+ipls_status ipls_partition_count(const void* d_in, size_t n, ipls_key_type t,
+                                 const ipls_model* h_model, uint64_t* d_offsets, void* stream) {
+  return partition_impl(kPartCount, d_in, nullptr, n, t, h_model, d_offsets, nullptr, nullptr,
+                        stream);
+}
+
+ipls_status ipls_partition_scatter_to(const void* d_in, size_t n, ipls_key_type t,
+                                      const ipls_model* h_model, const uint64_t* d_bucket_dst,
+                                      void* stream) {
+  return partition_impl(kPartScatterTo, d_in, nullptr, n, t, h_model, nullptr, nullptr,
+                        d_bucket_dst, stream);
 }
 
 const char* ipls_status_string(ipls_status s) {

@@ -724,6 +724,9 @@ struct LevelArgs {
   int check_nan;
   uint16_t* ids;         // partition_level only: per-key buckets
   uint64_t* single_offsets;  // partition_level only: k_eff+1 bucket boundaries
+  const uint64_t* bucket_dst;  // partition_scatter_to only (PEER kernels): bucket b's keys of this
+                               // array go to the words from address bucket_dst[b] on (any
+                               // device-accessible memory, e.g. a peer GPU's over NVLink)
   SegDesc* nsegs;
   ChunkDesc* nchunks;
   LevelCounters* nctr;
@@ -1327,6 +1330,10 @@ __host__ __device__ constexpr size_t scatter_stable_smem_bytes(uint32_t k) {
   return (size_t)kSTile * 8 + (size_t)kSTile * 2 + (size_t)2 * kSPairs * k * 4 + (size_t)k * 8 +
          (size_t)k * 4 * 2 + (size_t)k * 2 + 64;
 }
+// PEER variant: plus the k per-bucket destination bases
+__host__ __device__ constexpr size_t scatter_peer_smem_bytes(uint32_t k) {
+  return scatter_stable_smem_bytes(k) + (size_t)k * 8 + 8;
+}
 
 #ifdef IPLS_SCATTER_TIMING
 #define SC_TICK(N) do { if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_sc_phase[N], (unsigned long long)(t_ - t_prev_)); t_prev_ = t_; } } while (0)
@@ -1419,7 +1426,10 @@ __device__ __forceinline__ uint32_t scan_excl_1bar(uint32_t x, uint32_t* sw, uin
 // Rank modes of phase A in the stable kernel.
 constexpr int kRankAtomic = 0, kRankDense = 1, kRankMatch = 2;
 
-template <bool F64, int MODE>
+// PEER (the multi-GPU exchange fused into the scatter): every bucket has its own
+// destination base address (a.bucket_dst, copied to smem), so a run is written straight into
+// the buffer of the rank that owns the bucket; the run offsets are the chunk prefixes alone.
+template <bool F64, int MODE, bool PEER = false>
 __device__ void scatter_stable_chunk(const LevelArgs& a, uint64_t* __restrict__ dst_user,
                                      uint64_t* __restrict__ dst_scr, uint32_t c,
                                      const ChunkDesc& ch, const ModelDev& md,
@@ -1442,7 +1452,17 @@ __device__ void scatter_stable_chunk(const LevelArgs& a, uint64_t* __restrict__ 
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const uint32_t t = threadIdx.x;
   const uint32_t lt = lanemask_lt();
-  uint64_t* dst = chunk_runs<NT>(a, dst_user, dst_scr, c, ch.seg, runo);
+  uint64_t* dst = nullptr;
+  uint64_t** pdst = nullptr;  // PEER: per-bucket destination bases
+  if constexpr (PEER) {
+    pdst = reinterpret_cast<uint64_t**>((reinterpret_cast<uintptr_t>(multi + k) + 7) & ~(uintptr_t)7);
+    for (uint32_t b = t; b < k; b += NT) {
+      runo[b] = a.chunk_pre[(size_t)c * k + b];
+      pdst[b] = reinterpret_cast<uint64_t*>(a.bucket_dst[b]);
+    }
+  } else {
+    dst = chunk_runs<NT>(a, dst_user, dst_scr, c, ch.seg, runo);
+  }
   for (uint32_t b = t; b < k; b += NT) { seen[b] = 0; multi[b] = 0; }
   {  // both counter tables start cleared
     uint4* z = reinterpret_cast<uint4*>(tab0);
@@ -1653,7 +1673,8 @@ __device__ void scatter_stable_chunk(const LevelArgs& a, uint64_t* __restrict__ 
               if (!seen[b[j]]) { ref[b[j]] = v[j]; seen[b[j]] = 1; }
               else if (ref[b[j]] != v[j]) multi[b[j]] = 1;
             }
-            st_hint(dst + (uint32_t)(ao[j] + q), v[j], pol);
+            if constexpr (PEER) pdst[b[j]][(uint32_t)(ao[j] + q)] = v[j];
+            else st_hint(dst + (uint32_t)(ao[j] + q), v[j], pol);
           }
         }
       }
@@ -1870,6 +1891,20 @@ __global__ __launch_bounds__(kSThreads, 1) void k_scatter_stable(LevelArgs a, ui
     scatter_stable_chunk<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw);
   else
     scatter_stable_chunk<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
+}
+
+// The stable scatter with per-bucket destinations (ipls_partition_scatter_to): one segment,
+// every chunk stable, linear or EQ3 model.
+template <bool F64>
+__global__ __launch_bounds__(kSThreads, 1) void k_scatter_peer(LevelArgs a) {
+  const uint32_t c = blockIdx.x;
+  const ChunkDesc ch = a.chunks[c];
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const ModelDev md = a.models[ch.seg];
+  if (md.kind == kModelEq3)
+    scatter_stable_chunk<F64, kModelEq3, true>(a, nullptr, nullptr, c, ch, md, smraw);
+  else
+    scatter_stable_chunk<F64, kModelLinear, true>(a, nullptr, nullptr, c, ch, md, smraw);
 }
 
 template <bool F64, bool TREE>

@@ -24,6 +24,16 @@ sort.  A global array is the concatenation, in rank order, of every rank's shard
    is the one a one-GPU sort of the concatenation fits (the regrouped bucket is exactly the
    stable level-0 child of the global array).
 
+Fused exchange (`dist_sort(..., fused=True)`, the default on NCCL when the top-level model is
+linear): steps 3 and 5's partition + all-to-all + regroup (three passes over the keys) become
+one.  Every rank counts its buckets (`ipls_partition_count`), the counts are all-gathered,
+`fused_plan` gives every (source, bucket) its place in the owner's receive buffer
+(bucket-major, then source rank: exactly `ipls_regroup_runs`' layout), and the stable scatter
+(`ipls_partition_scatter_to`) stores every run straight into that buffer -- the owner's
+memory mapped into the source's address space (torch symmetric memory: CUDA VMM allocations
+shared over NVLink / NVSwitch).  One barrier, then the local sort.  EQ3 top levels (degenerate
+global samples: a bucket shared between ranks) keep the all-to-all path.
+
 Failures agree: every rank all-reduces (MAX) its status before each collective that follows
 a step that can fail (fit, partition, the receive allocation) and after the local sort, and
 all ranks raise together.
@@ -42,8 +52,9 @@ from typing import List, Optional
 
 import numpy as np
 
-from . import (DEFAULT_SEED, MODEL_EQ3, IPLSError, Model, assign_cuts, fit_fmcd, partition_level,
-               regroup_runs, sample_size, sample_strata, sort, sort_segments, _key_type_of)
+from . import (DEFAULT_SEED, MODEL_EQ3, IPLSError, Model, assign_cuts, fit_fmcd, partition_count,
+               partition_level, partition_scatter_to, regroup_runs, sample_size, sample_strata,
+               sort, sort_segments, _key_type_of)
 
 
 class CudaOps:
@@ -78,6 +89,22 @@ class CudaOps:
         out = torch.empty_like(keys)
         off, _ = partition_level(keys, out, model, key_type=key_type, stream=self.stream)
         return out, [int(x) for x in off.cpu().tolist()]
+
+    def partition_count(self, keys, model: Model, key_type: int):
+        """Bucket boundaries of the shard's stable partition (host list of k_eff + 1 ints)."""
+        off = partition_count(keys, model, key_type=key_type, stream=self.stream)
+        return [int(x) for x in off.cpu().tolist()]
+
+    def scatter_to(self, keys, model: Model, key_type: int, addresses) -> int:
+        """Stable scatter with one destination address per bucket (host list of ints; own or
+        peer memory); returns the status."""
+        import torch
+        try:
+            dst = torch.tensor(addresses, dtype=torch.int64, device=keys.device)
+            partition_scatter_to(keys, model, dst, key_type=key_type, stream=self.stream)
+            return 0
+        except IPLSError as e:
+            return e.status
 
     def regroup(self, runs, counts: np.ndarray):
         """The G received runs (counts: G x nb) into bucket-major order (ipls_regroup_runs)."""
@@ -135,6 +162,50 @@ def exchange_plan(cnt: np.ndarray, G: int, splittable=None):
     return cuts, bounds, M
 
 
+def fused_plan(cnt: np.ndarray, G: int):
+    """The fused exchange's plan from the G x k per-rank bucket counts (host; no bucket is
+    split between ranks).  Returns (cuts, bounds, owner, offset, recv):
+    cuts, bounds as exchange_plan's; owner[b] = the rank that receives bucket b; offset[s, b] =
+    the position, in owner[b]'s receive buffer, of source s's first key of bucket b -- the
+    buffer holds the owner's buckets in order, each as source 0's keys, then source 1's, ...
+    (the stable partition of the global array restricted to those buckets); recv[d] = keys
+    rank d receives."""
+    cnt = np.asarray(cnt, dtype=np.int64)
+    total = cnt.sum(axis=0)
+    cuts = assign_cuts(total, G, None)
+    pre = np.concatenate([[0], np.cumsum(total)])
+    bounds = [int(np.searchsorted(pre, c, side="left")) for c in cuts[:G]] + [len(total)]
+    owner = np.zeros(len(total), dtype=np.int64)
+    for d in range(G):
+        owner[bounds[d]:bounds[d + 1]] = d
+    base = pre[:-1] - pre[np.asarray(bounds)[owner]]          # bucket b's region in its owner
+    offset = base[None, :] + np.cumsum(cnt, axis=0) - cnt      # + the lower sources' keys of b
+    recv = [int(pre[bounds[d + 1]] - pre[bounds[d]]) for d in range(G)]
+    return cuts, bounds, owner, offset, recv
+
+
+class SymmPeers:
+    """Receive buffers every rank of the group can store into: torch symmetric memory (CUDA
+    VMM allocations exchanged between the processes and mapped over NVLink / NVSwitch)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.group = group if group is not None else dist.group.WORLD
+        self.handle = None
+
+    def alloc(self, nelems: int, device):
+        """A buffer of nelems int64 on every rank (same size everywhere) -> (this rank's
+        tensor, the list of every rank's base address as seen from this rank)."""
+        import torch
+        import torch.distributed._symmetric_memory as symm
+        t = symm.empty(max(1, nelems), dtype=torch.int64, device=device)
+        self.handle = symm.rendezvous(t, self.group)
+        return t, [int(p) for p in self.handle.buffer_ptrs]
+
+    def barrier(self):
+        self.handle.barrier()
+
+
 def _all_gather_int64(vals, group, device):
     """All-gather a 1-D list of ints (same length on every rank) -> [G, len] numpy."""
     import torch
@@ -148,7 +219,8 @@ def _all_gather_int64(vals, group, device):
 
 def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SEED,
               key_type: Optional[int] = None, group=None, ops=None,
-              marks: Optional[list] = None) -> DistResult:
+              marks: Optional[list] = None, fused: Optional[bool] = None,
+              peers=None) -> DistResult:
     """Sort the global array whose rank-ordered shards the ranks of `group` hold.
 
     keys: this rank's shard (CUDA tensor, float64 or (u)int64 holding uint64 bits; left
@@ -156,6 +228,9 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
     any rank's step fails (e.g. a NaN key anywhere: IPLS_ERR_NAN_KEY).
     marks: optional list; (phase name, CUDA event) pairs are appended at the phase
     boundaries (tools/time_dist.py).
+    fused: scatter straight into the owners' receive buffers over peer memory instead of
+    partition + all-to-all + regroup (module docstring); default: on for the NCCL backend.
+    peers: the object that provides those buffers (default SymmPeers(group)).
     """
     import torch
     import torch.distributed as dist
@@ -205,6 +280,11 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
         smp = smp_c.to(dev)
         model, status = attempt(lambda: ops.fit(smp, kt, k))          # step 2 (same on all ranks)
     mark("sample+fit")
+    if fused is None:
+        fused = dist.get_backend(group) == "nccl"
+    if fused and model is not None and status == 0 and model.kind != MODEL_EQ3:
+        return _fused_tail(keys, model, kt, k, base_case, seed, group, ops, peers, agree,
+                           attempt, mark, cdev, G, r, gm)
     if model is not None and status == 0:
         po, status = attempt(lambda: ops.partition(keys, model, kt))  # step 3
         part, off = po if po is not None else (keys, [0, keys.numel()])
@@ -248,4 +328,45 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
     return DistResult(out, bounds, model, total, cuts[r], gm, cuts)
 
 
-__all__ = ["dist_sort", "DistResult", "CudaOps"]
+def _fused_tail(keys, model, kt, k, base_case, seed, group, ops, peers, agree, attempt, mark,
+                cdev, G, r, gm) -> DistResult:
+    """Steps 3'-5' of the fused exchange (module docstring)."""
+    import torch
+    dev = keys.device
+    off, status = attempt(lambda: ops.partition_count(keys, model, kt))           # step 3'
+    st = agree(status)
+    if st:
+        raise IPLSError(st, "in the distributed partition")
+    ke = len(off) - 1
+    cnt = _all_gather_int64([off[b + 1] - off[b] for b in range(ke)], group, cdev)
+    total = cnt.sum(axis=0)
+    mark("partition")
+    cuts, bounds, owner, offset, recv = fused_plan(cnt, G)                        # step 4
+    peers = peers if peers is not None else SymmPeers(group)
+    status = 1 if max(recv) > 0xFFFFFFFF else 0  # beyond the ABI's 2^32 - 1 keys per call
+    bp = None
+    if status == 0:
+        bp, status = attempt(lambda: peers.alloc(max(recv), dev))
+    st = agree(status)
+    if st:
+        raise IPLSError(st, "before the exchange")
+    buf, ptrs = bp
+    addr = [ptrs[int(owner[b])] + 8 * int(offset[r, b]) for b in range(ke)]
+    peers.barrier()   # every receive buffer exists (and nobody still reads an earlier one)
+    status = ops.scatter_to(keys, model, kt, addr)                                # step 5'
+    st = agree(status)
+    if st:
+        raise IPLSError(st, "in the exchange")
+    peers.barrier()   # every source's stores have landed (scatter_to synchronises its stream)
+    mark("plan+exchange")
+    out = buf[:recv[r]].view(keys.dtype)
+    sizes = total[bounds[r]:bounds[r + 1]]
+    status = ops.sort_segments(out, kt, k, base_case, seed, sizes, 1, cuts[r])
+    mark("local sort")
+    st = agree(status)
+    if st:
+        raise IPLSError(st, "in the distributed sort")
+    return DistResult(out, bounds, model, total, cuts[r], gm, cuts)
+
+
+__all__ = ["dist_sort", "DistResult", "CudaOps", "SymmPeers", "fused_plan"]

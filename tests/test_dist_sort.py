@@ -76,6 +76,26 @@ class OracleOps:
         out, off, _ = oracle.partition(a, m.a, m.b, m.k, m.kind, m.pivot_ok)
         return torch.from_numpy(out.view(np.int64).copy()), [int(x) for x in off]
 
+    peers = None  # fused exchange: the ShmPeers whose views stand for peer memory
+
+    def partition_count(self, keys, m, kt):
+        a = self._np(keys, kt)
+        _, off, _ = oracle.partition(a, m.a, m.b, m.k, m.kind, m.pivot_ok)
+        return [int(x) for x in off]
+
+    def scatter_to(self, keys, m, kt, addresses):
+        """Stable partition by the oracle, every bucket copied to its "address" (ShmPeers:
+        rank << 44 | byte offset in that rank's shared-memory buffer)."""
+        a = self._np(keys, kt)
+        out, off, _ = oracle.partition(a, m.a, m.b, m.k, m.kind, m.pivot_ok)
+        bits = out.view(np.int64)
+        for b, ad in enumerate(addresses):
+            c = int(off[b + 1] - off[b])
+            if c:
+                d, o = ad >> 44, (ad & ((1 << 44) - 1)) // 8
+                self.peers.views[d][o:o + c] = bits[int(off[b]):int(off[b + 1])]
+        return 0
+
     def regroup(self, runs, counts):
         """Bucket-major order of the G received runs (the reference for ipls_regroup_runs)."""
         bits = runs.view(torch.int64).numpy()
@@ -95,6 +115,44 @@ class OracleOps:
         return self.sort(t, kt, k, base_case, seed)
 
 
+class ShmPeers:
+    """Test stand-in for SymmPeers: every rank's receive buffer is a named POSIX shared-memory
+    block the other processes attach to; an "address" is rank << 44 | byte offset."""
+
+    def __init__(self, tag, rank, world):
+        self.tag, self.rank, self.world = tag, rank, world
+        self.shms, self.views = [], []
+
+    def alloc(self, nelems, device):
+        import torch.distributed as dist
+        from multiprocessing import shared_memory
+        n = max(1, nelems)
+        own = shared_memory.SharedMemory(create=True, size=8 * n, name=f"{self.tag}_{self.rank}")
+        dist.barrier()
+        for d in range(self.world):
+            shm = own if d == self.rank else shared_memory.SharedMemory(name=f"{self.tag}_{d}")
+            self.shms.append(shm)
+            self.views.append(np.ndarray((n,), np.int64, buffer=shm.buf))
+        self.views[self.rank][:] = -1
+        return torch.from_numpy(self.views[self.rank]), [d << 44 for d in range(self.world)]
+
+    def barrier(self):
+        import torch.distributed as dist
+        dist.barrier()
+
+    def close(self):
+        import torch.distributed as dist
+        self.views = []
+        dist.barrier()
+        for d, shm in enumerate(self.shms):
+            try:
+                shm.close()
+            except BufferError:
+                pass
+            if d == self.rank:
+                shm.unlink()
+
+
 def _shards(kind, n, G, seed):
     rng = np.random.default_rng(seed)
     a = datagen.fuzz_array(rng, n, "normal" if kind == "nan_one" else kind)
@@ -106,32 +164,39 @@ def _shards(kind, n, G, seed):
     return a, np.split(a, cuts)
 
 
-def _worker(rank, world, port, q, kind, n, k, B, seed):
+def _worker(rank, world, port, q, kind, n, k, B, seed, fused=False):
     os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
     import torch.distributed as dist
     from paper_2208_06902_b200.distributed import dist_sort
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    peers = ShmPeers(f"ipls{port}", rank, world) if fused else None
     try:
         _, shards = _shards(kind, n, world, seed)
         mine = torch.from_numpy(shards[rank].view(np.int64).copy())
         kt = ipls.KEY_F64 if shards[rank].dtype == np.float64 else ipls.KEY_U64
+        ops = OracleOps()
+        ops.peers = peers
         try:
-            res = dist_sort(mine, k=k, base_case=B, key_type=kt, ops=OracleOps())
+            res = dist_sort(mine, k=k, base_case=B, key_type=kt, ops=ops, fused=fused,
+                            peers=peers)
             m = res.model
             q.put((rank, "ok", res.keys.numpy().copy(), res.bounds, res.counts,
                    None if m is None else (m.a, m.b, m.D, m.kind, m.pivot_ok),
                    res.global_begin, res.global_n))
         except ipls.IPLSError as e:
             q.put((rank, "err", e.status))
+        if peers is not None and peers.shms:
+            del res
+            peers.close()
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, kind, n, k=64, B=64, seed=3):
+def _run(world, kind, n, k=64, B=64, seed=3, fused=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, q, kind, n, k, B, seed))
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q, kind, n, k, B, seed, fused))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -178,6 +243,53 @@ def test_dist_sort_matches_oracle_level0(world, kind):
         rk = r[0]
         assert r[6] == cuts[rk] and len(r[2]) == cuts[rk + 1] - cuts[rk]
         assert r[7] == n
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("kind", ["normal", "few_distinct", "u64_above_2_53", "all_equal"])
+def test_dist_sort_fused_exchange_equals_all_to_all_path(world, kind):
+    """The fused exchange (count, plan, scatter into the owners' buffers: here shared memory
+    standing for peer memory) gives every rank exactly what partition + all-to-all + regroup
+    gives it (an EQ3 top level, all_equal, takes that path itself)."""
+    n, k, B, seed = 30000, 64, 64, 3
+    a, _ = _shards(kind, n, world, seed)
+    ref = _run(world, kind, n, k, B, seed)
+    res = _run(world, kind, n, k, B, seed, fused=True)
+    assert all(r[1] == "ok" for r in res)
+    for x, y in zip(ref, res):
+        assert x[2].tobytes() == y[2].tobytes()
+        assert x[3] == y[3] and np.array_equal(x[4], y[4]) and x[5:] == y[5:]
+    got = np.concatenate([r[2] for r in res]).view(a.dtype)
+    assert got.tobytes() == a[np.argsort(oracle.ordering_keys(a), kind="stable")].tobytes()
+
+
+def test_fused_plan_places_the_global_stable_partition():
+    """fused_plan against the definition: rank d's buffer, filled source by source at
+    offset[s, b], is the stable partition of the concatenated array restricted to d's
+    buckets."""
+    from paper_2208_06902_b200.distributed import exchange_plan, fused_plan
+    rng = np.random.default_rng(11)
+    for trial in range(60):
+        G, k = int(rng.integers(1, 6)), int(rng.integers(3, 12))
+        shards = [rng.integers(0, k, int(rng.integers(0, 40))) for _ in range(G)]  # bucket ids
+        tags = [np.arange(len(sh)) + 1000 * s for s, sh in enumerate(shards)]     # key identity
+        cnt = np.array([np.bincount(sh, minlength=k) for sh in shards])
+        cuts, bounds, owner, offset, recv = fused_plan(cnt, G)
+        c2, b2, M = exchange_plan(cnt, G, None)
+        assert cuts == c2 and bounds == b2 and recv == [int(m.sum()) for m in M]
+        bufs = [np.full(recv[d], -1, np.int64) for d in range(G)]
+        for s in range(G):
+            order = np.argsort(shards[s], kind="stable")
+            off = np.concatenate([[0], np.cumsum(cnt[s])])
+            for b in range(k):
+                run = tags[s][order][off[b]:off[b + 1]]
+                o = int(offset[s, b])
+                bufs[int(owner[b])][o:o + len(run)] = run
+        allb, allt = np.concatenate(shards), np.concatenate(tags)
+        glob = allt[np.argsort(allb, kind="stable")]
+        assert np.array_equal(np.concatenate(bufs), glob)
+        for d in range(G):
+            assert len(bufs[d]) == cuts[d + 1] - cuts[d]
 
 
 def test_dist_sort_tiny_and_nan():

@@ -111,6 +111,85 @@ def test_dist_sort_one_rank_nccl(ipls, nccl1, kind, n):
             assert m.kind == ipls.MODEL_EQ3 and m.pivot_ok == r0.pivot_ok
 
 
+@pytest.mark.parametrize("kind,n", [("normal", 2_000_000), ("lognormal", 300_000),
+                                    ("few_distinct", 500_000), ("u64_above_2_53", 400_000),
+                                    ("all_equal", 100_000), ("uniform", 5)])
+def test_dist_sort_fused_one_rank_nccl(ipls, nccl1, kind, n):
+    """The fused exchange in a real one-rank NCCL group: the receive buffer is torch symmetric
+    memory and the scatter stores into it through the address the rendezvous returns."""
+    from paper_2208_06902_b200.distributed import dist_sort
+    a = datagen.fuzz_array(np.random.default_rng(n), n, kind)
+    src = dev(a)
+    if a.dtype == np.float64:
+        src = src.view(torch.float64)
+    before = src.clone()
+    res = dist_sort(src, k=1024, base_case=4096, fused=True)
+    assert torch.equal(src, before)
+    want = a[np.argsort(oracle.ordering_keys(a), kind="stable")]
+    assert res.keys.cpu().numpy().tobytes() == want.tobytes()
+    ref = dist_sort(src, k=1024, base_case=4096, fused=False)
+    assert torch.equal(ref.keys.view(torch.int64), res.keys.view(torch.int64))
+    assert ref.bounds == res.bounds and ref.cuts == res.cuts
+
+
+def _model_of(ipls, r0, k):
+    if r0.kind == oracle.MODEL_LINEAR:
+        return ipls.Model(r0.A, r0.B, k, r0.D, ipls.MODEL_LINEAR, int(r0.capped), 0, False)
+    return ipls.Model(0.0, 0.0, 3, 0, ipls.MODEL_EQ3, 0, int(r0.pivot_ok), True)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+@pytest.mark.parametrize("kind,n,k", [("normal", 3_000_000, 1024), ("lognormal", 70_001, 256),
+                                      ("u64_above_2_53", 400_000, 1024),
+                                      ("few_distinct", 200_000, 64), ("all_equal", 50_000, 256),
+                                      ("normal", 5000, 16)])
+def test_partition_count_and_scatter_to_simulated_ranks(ipls, G, kind, n, k):
+    """ipls_partition_count + ipls_partition_scatter_to on the shards of one array (one GPU,
+    one independent call per simulated rank, the G receive buffers being local tensors): every
+    shard's offsets are the oracle's stable partition's, and the receive buffers, concatenated
+    in rank order, are the oracle's stable partition of the WHOLE array by the top-level
+    model (the bytes partition + all-to-all + regroup deliver), bit for bit."""
+    from paper_2208_06902_b200.distributed import fused_plan
+    rng = np.random.default_rng(n + G + k)
+    a = datagen.fuzz_array(rng, n, kind)
+    r0 = oracle.sort(a.copy(), k=k, base_case=64, trace=True).records[0]
+    m = _model_of(ipls, r0, k)
+    kt = 0 if a.dtype == np.float64 else 1
+    cuts = np.sort(rng.integers(0, n + 1, G - 1))
+    if G > 2:
+        cuts[1] = cuts[0]  # an empty shard
+    shards = np.split(a, cuts)
+    tsh = [dev(sh) for sh in shards]
+    cnt = []
+    for sh, t in zip(shards, tsh):
+        off = ipls.partition_count(t, m, key_type=kt).cpu().numpy()
+        _, want_off, _ = oracle.partition(sh, m.a, m.b, m.k, m.kind, m.pivot_ok)
+        assert np.array_equal(off.astype(np.uint64), np.asarray(want_off, dtype=np.uint64))
+        cnt.append(np.diff(off))
+    cnt = np.array(cnt)
+    _, bounds, owner, offset, recv = fused_plan(cnt, G)
+    bufs = [torch.full((max(1, recv[d]),), -1, dtype=torch.int64, device="cuda") for d in range(G)]
+    for s, t in enumerate(tsh):
+        before = t.clone()
+        addr = torch.tensor([bufs[int(owner[b])].data_ptr() + 8 * int(offset[s, b])
+                             for b in range(cnt.shape[1])], dtype=torch.int64, device="cuda")
+        ipls.partition_scatter_to(t, m, addr, key_type=kt)
+        assert torch.equal(t, before)  # the source shard is left unmodified
+    got = np.concatenate([bufs[d][:recv[d]].cpu().numpy() for d in range(G)])
+    want, _, _ = oracle.partition(a, m.a, m.b, m.k, m.kind, m.pivot_ok)
+    assert got.tobytes() == want.tobytes()
+    assert np.array_equal(cnt.sum(axis=0).astype(np.uint64), r0.counts)
+
+
+def test_partition_scatter_to_rejects_bad_arguments(ipls):
+    t = dev(np.random.default_rng(0).random(1000))
+    m = ipls.Model(1.0, 0.0, 8, 1, ipls.MODEL_LINEAR, 0, 0, False)
+    with pytest.raises(ValueError):
+        ipls.partition_scatter_to(t, m, torch.zeros(4, dtype=torch.int64, device="cuda"))
+    assert ipls.lib().ipls_partition_scatter_to(t.data_ptr(), 1000, 0, None, None, None) == 1
+    assert ipls.lib().ipls_partition_count(t.data_ptr(), 1000, 0, None, None, None) == 1
+
+
 def test_dist_sort_nan_raises(ipls, nccl1):
     from paper_2208_06902_b200.distributed import dist_sort
     a = np.random.default_rng(0).normal(size=50000)
