@@ -211,14 +211,16 @@ def bench_reference(args):
 
 def bench_dist(args, world, rank, local):
     """N ranks, one array: the workload sharded in rank order (n/N keys each), sorted by
-    dist_sort (global sample + shared FMCD model, stable partition, count
-    all-gather, range plan, one NCCL all-to-all, regroup, local sorts resumed at level 1).
+    dist_sort (global sample + shared FMCD model, bucket counts, count
+    all-gather, range plan, the stable scatter straight into the owners' receive buffers over
+    peer memory (else partition + one NCCL all-to-all + regroup), local sorts resumed at
+    level 1).
     Strong scaling: value = n / max over ranks of the step time."""
     import torch
     import torch.distributed as dist
     import paper_2208_06902_b200 as ipls
     from paper_2208_06902_b200 import datagen
-    from paper_2208_06902_b200.distributed import dist_sort
+    from paper_2208_06902_b200.distributed import SymmPeers, dist_sort
     if world == 1 and not dist.is_initialized():
         import socket
         sk = socket.socket(); sk.bind(("127.0.0.1", 0)); port = sk.getsockname()[1]; sk.close()
@@ -238,12 +240,28 @@ def bench_dist(args, world, rank, local):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()
 
+    # The exchange fused into the scatter (peer stores into symmetric-memory receive buffers,
+    # reused between steps); if the peer buffers cannot be set up every rank raises together
+    # (status 6) and the run uses the NCCL all-to-all path instead, and says so.
+    dkw = {"fused": True, "peers": SymmPeers(reuse=True)}
+    exchange = "fused: stable scatter straight into the owners' symmetric-memory buffers"
+    try:
+        if args.exchange == "nccl":
+            raise ipls.IPLSError(6, "--exchange nccl")
+        work.copy_(shard)
+        dist_sort(work, k=cfg.k, base_case=cfg.base_case, **dkw)
+    except ipls.IPLSError as e:
+        if e.status != 6:
+            raise
+        dkw = {"fused": False}
+        exchange = f"one NCCL all-to-all + regroup (fused exchange unavailable: {e})"
+
     def one(evs=None):
         work.copy_(shard)
         flush.fill_(1)
         if evs is not None:
             evs[0].record(st)
-        res = dist_sort(work, k=cfg.k, base_case=cfg.base_case)
+        res = dist_sort(work, k=cfg.k, base_case=cfg.base_case, **dkw)
         if evs is not None:
             evs[1].record(st)
         return res
@@ -288,6 +306,7 @@ def bench_dist(args, world, rank, local):
     achieved = d_bytes / (d_ms / 1e3) / 1e9
     # e2e: the shard from pinned host memory, dist_sort, the result back to host
     hsh = torch.from_numpy(a[lo:hi].view(np.int64).copy()).pin_memory()
+    hout = torch.empty(2 * (hi - lo) + 1024, dtype=torch.int64).pin_memory()  # the rank's range
     e2e = []
     for i in range(args.e2e_steps + 1):
         dist.barrier()
@@ -296,8 +315,12 @@ def bench_dist(args, world, rank, local):
         w = hsh.to(dev, non_blocking=True)
         if a.dtype == np.float64:
             w = w.view(torch.float64)
-        r = dist_sort(w, k=cfg.k, base_case=cfg.base_case)
-        back = r.keys.cpu()
+        r = dist_sort(w, k=cfg.k, base_case=cfg.base_case, **dkw)
+        got = r.keys.view(torch.int64)
+        if got.numel() <= hout.numel():
+            hout[:got.numel()].copy_(got, non_blocking=True)
+        else:
+            back = got.cpu()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if i > 0:
@@ -315,8 +338,9 @@ def bench_dist(args, world, rank, local):
             "dtype": "f64" if a.dtype == np.float64 else "u64", "data": "synthetic",
             "config": {
                 "workload": f"{args.config}: {cfg.desc}, n={n}, k={cfg.k}, base_case={cfg.base_case}",
-                "parallelism": f"dist_sort over {world} rank(s): shards of n/{world} keys, one "
-                               "NCCL all-to-all, local sorts resumed at level 1",
+                "parallelism": f"dist_sort over {world} rank(s): shards of n/{world} keys, "
+                               "local sorts resumed at level 1",
+                "exchange": exchange,
                 "l2": "shard restored (D2D) and a 256 MB buffer written before every step",
                 "timing": "CUDA events around each dist_sort call; median over steps; max over ranks",
                 "sort_roofline_model": {"bytes_per_key": 16 * (Lstar + 1),
@@ -357,6 +381,9 @@ def main():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: every rank sorts its own copy of the workload (weak scaling) "
                          "instead of dist_sort on one array sharded over the ranks")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="dist_sort's exchange: the scatter fused with peer stores (default) or "
+                         "partition + NCCL all-to-all + regroup")
     ap.add_argument("--dist", action="store_true",
                     help="run dist_sort even at N = 1 (a one-rank NCCL group; for testing)")
     ap.add_argument("--traffic", type=float, default=None,

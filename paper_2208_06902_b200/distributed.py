@@ -188,18 +188,27 @@ class SymmPeers:
     """Receive buffers every rank of the group can store into: torch symmetric memory (CUDA
     VMM allocations exchanged between the processes and mapped over NVLink / NVSwitch)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, reuse: bool = False):
+        """reuse: keep the buffer between calls and hand it out again while it is large enough
+        (the allocation and its rendezvous cost milliseconds).  The caller then owns the
+        consequence: a dist_sort result is a view of the buffer and is overwritten by the next
+        dist_sort that uses this object."""
         import torch.distributed as dist
         self.group = group if group is not None else dist.group.WORLD
         self.handle = None
+        self.reuse = reuse
+        self.buf = None
 
     def alloc(self, nelems: int, device):
         """A buffer of nelems int64 on every rank (same size everywhere) -> (this rank's
         tensor, the list of every rank's base address as seen from this rank)."""
         import torch
         import torch.distributed._symmetric_memory as symm
+        if self.reuse and self.buf is not None and self.buf.numel() >= nelems:
+            return self.buf, [int(p) for p in self.handle.buffer_ptrs]
         t = symm.empty(max(1, nelems), dtype=torch.int64, device=device)
         self.handle = symm.rendezvous(t, self.group)
+        self.buf = t if self.reuse else None
         return t, [int(p) for p in self.handle.buffer_ptrs]
 
     def barrier(self):
@@ -345,13 +354,20 @@ def _fused_tail(keys, model, kt, k, base_case, seed, group, ops, peers, agree, a
     peers = peers if peers is not None else SymmPeers(group)
     status = 1 if max(recv) > 0xFFFFFFFF else 0  # beyond the ABI's 2^32 - 1 keys per call
     bp = None
+    def alloc():
+        try:
+            return peers.alloc(max(recv), dev)
+        except (IPLSError, torch.cuda.OutOfMemoryError):
+            raise
+        except Exception as e:  # no peer access, symmetric memory unavailable, ...
+            raise IPLSError(6, f"peer receive buffers: {e}")
     if status == 0:
-        bp, status = attempt(lambda: peers.alloc(max(recv), dev))
+        bp, status = attempt(alloc)
     st = agree(status)
     if st:
         raise IPLSError(st, "before the exchange")
     buf, ptrs = bp
-    addr = [ptrs[int(owner[b])] + 8 * int(offset[r, b]) for b in range(ke)]
+    addr = (np.asarray(ptrs, dtype=np.int64)[owner] + 8 * offset[r]).tolist()
     peers.barrier()   # every receive buffer exists (and nobody still reads an earlier one)
     status = ops.scatter_to(keys, model, kt, addr)                                # step 5'
     st = agree(status)

@@ -13,7 +13,7 @@ import torch.distributed as dist
 
 import paper_2208_06902_b200 as ipls
 from paper_2208_06902_b200 import datagen
-from paper_2208_06902_b200.distributed import dist_sort
+from paper_2208_06902_b200.distributed import SymmPeers, dist_sort
 
 s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
 os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
@@ -40,21 +40,26 @@ def timed(fn):
 
 
 ms1, _ = timed(lambda: ipls.sort(work, k=cfg.k, base_case=cfg.base_case))
-msd, res = timed(lambda: dist_sort(work, k=cfg.k, base_case=cfg.base_case))
-ok = torch.equal(res.keys, torch.sort(src)[0])
-work.copy_(src); torch.cuda.synchronize()
-ipls.profile_reset(); ipls.profile_enable(True)
-dist_sort(work, k=cfg.k, base_case=cfg.base_case)
-ipls.profile_enable(False)
-for _ in range(3):
+want = torch.sort(src)[0]
+for label, kw in [("all-to-all path", dict(fused=False)),
+                  ("fused exchange, buffer allocated per call", dict(fused=True)),
+                  ("fused exchange, buffer reused", dict(fused=True, peers=SymmPeers(reuse=True)))]:
+    msd, res = timed(lambda: dist_sort(work, k=cfg.k, base_case=cfg.base_case, **kw))
+    ok = torch.equal(res.keys, want)
     work.copy_(src); torch.cuda.synchronize()
-    marks = []
-    dist_sort(work, k=cfg.k, base_case=cfg.base_case, marks=marks)
-    torch.cuda.synchronize()
-print("  phases: " + "  ".join(f"{n}:{marks[i - 1][1].elapsed_time(e):.3f}ms"
-                               for i, (n, e) in enumerate(marks) if i), flush=True)
-print("  library kernels in one dist_sort: " + "  ".join(
-    f"{k}:{v[1]:.3f}ms/{v[0]}" for k, v in sorted(ipls.profile_read().items())), flush=True)
-print(f"{name}: one-GPU sort {ms1:.3f} ms, dist_sort (1 rank) {msd:.3f} ms "
-      f"(+{msd - ms1:.3f} ms top-level pass), sorted={ok}", flush=True)
+    ipls.profile_reset(); ipls.profile_enable(True)
+    dist_sort(work, k=cfg.k, base_case=cfg.base_case, **kw)
+    ipls.profile_enable(False)
+    prof = ipls.profile_read()
+    for _ in range(3):
+        work.copy_(src); torch.cuda.synchronize()
+        marks = []
+        dist_sort(work, k=cfg.k, base_case=cfg.base_case, marks=marks, **kw)
+        torch.cuda.synchronize()
+    print(f"{name}, {label}: one-GPU sort {ms1:.3f} ms, dist_sort (1 rank) {msd:.3f} ms "
+          f"(+{msd - ms1:.3f} ms top-level pass), sorted={ok}", flush=True)
+    print("  phases: " + "  ".join(f"{n}:{marks[i - 1][1].elapsed_time(e):.3f}ms"
+                                   for i, (n, e) in enumerate(marks) if i), flush=True)
+    print("  library kernels in one dist_sort: " + "  ".join(
+        f"{k}:{v[1]:.3f}ms/{v[0]}" for k, v in sorted(prof.items())), flush=True)
 dist.destroy_process_group()
