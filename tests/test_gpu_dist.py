@@ -181,6 +181,44 @@ def test_partition_count_and_scatter_to_simulated_ranks(ipls, G, kind, n, k):
     assert np.array_equal(cnt.sum(axis=0).astype(np.uint64), r0.counts)
 
 
+def test_fused_exchange_full_size_c2(ipls):
+    """C2 at full size (1e8 keys) cut into 8 even shards, as bench.py --gpus 8 shards it: the
+    eight receive buffers filled by ipls_partition_scatter_to are, concatenated, the oracle's
+    stable partition of the whole array by the oracle's level-0 model (SHA-256 of the bytes),
+    and the plan's ranges are the buckets' global prefix sums."""
+    import hashlib
+    from paper_2208_06902_b200.distributed import fused_plan
+    G = 8
+    cfg = datagen.CONFIGS["C2"]
+    a = datagen.generate("C2")
+    n = a.size
+    S = oracle.sample_size(n, cfg.k)
+    pos = oracle.sample_positions(ipls.DEFAULT_SEED, 0, 0, n, S).astype(np.int64)
+    smp = np.sort(a[pos])
+    f = oracle.fit_fmcd(smp, cfg.k)
+    assert not f.degenerate
+    m = ipls.Model(f.A, f.B, cfg.k, f.D, ipls.MODEL_LINEAR, int(f.capped), 0, False)
+    want, want_off, _ = oracle.partition(a, m.a, m.b, m.k, m.kind, 0)
+    want_sha = hashlib.sha256(want.tobytes()).hexdigest()
+    del want
+    tsh = [dev(a[n * r // G: n * (r + 1) // G]) for r in range(G)]
+    del a
+    cnt = np.array([np.diff(ipls.partition_count(t, m, key_type=0).cpu().numpy()) for t in tsh])
+    assert np.array_equal(np.concatenate([[0], np.cumsum(cnt.sum(axis=0))]).astype(np.uint64),
+                          np.asarray(want_off, dtype=np.uint64))
+    cuts, bounds, owner, offset, recv = fused_plan(cnt, G)
+    assert sum(recv) == n and max(recv) < 1.2 * n / G   # C2's buckets balance the ranks
+    bufs = [torch.empty(recv[d], dtype=torch.int64, device="cuda") for d in range(G)]
+    base = np.array([bufs[int(owner[b])].data_ptr() for b in range(cfg.k)], dtype=np.int64)
+    for s, t in enumerate(tsh):
+        addr = torch.from_numpy(base + 8 * offset[s]).cuda()
+        ipls.partition_scatter_to(t, m, addr, key_type=0)
+    h = hashlib.sha256()
+    for d in range(G):
+        h.update(bufs[d].cpu().numpy().tobytes())
+    assert h.hexdigest() == want_sha
+
+
 def test_partition_scatter_to_rejects_bad_arguments(ipls):
     t = dev(np.random.default_rng(0).random(1000))
     m = ipls.Model(1.0, 0.0, 8, 1, ipls.MODEL_LINEAR, 0, 0, False)
