@@ -691,7 +691,10 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     }
     {
       IPLS_PROF("scatter", 16.0 * level_keys);
-      launch_scatter<F64>(nchunk, st, la, keys, scr, p.tree);
+      // A segment of more than k * B keys has a child above B, so it is not terminal: the
+      // root level of a large sort skips the (empty) terminal launch.
+      const bool no_terminal = iter == 0 && !init && n > (uint64_t)k * p.B;
+      launch_scatter<F64>(nchunk, st, la, keys, scr, p.tree, no_terminal);
     }
     {
       IPLS_PROF("emit", 0);

@@ -24,8 +24,8 @@ sort.  A global array is the concatenation, in rank order, of every rank's shard
    is the one a one-GPU sort of the concatenation fits (the regrouped bucket is exactly the
    stable level-0 child of the global array).
 
-Fused exchange (`dist_sort(..., fused=True)`, the default on NCCL when the top-level model is
-linear): steps 3 and 5's partition + all-to-all + regroup (three passes over the keys) become
+Fused exchange (`dist_sort(..., peers=SymmPeers(reuse=True))` or `fused=True`, for a linear
+top-level model; bench.py's multi-GPU path): steps 3 and 5's partition + all-to-all + regroup (three passes over the keys) become
 one.  Every rank counts its buckets (`ipls_partition_count`), the counts are all-gathered,
 `fused_plan` gives every (source, bucket) its place in the owner's receive buffer
 (bucket-major, then source rank: exactly `ipls_regroup_runs`' layout), and the stable scatter
@@ -238,8 +238,10 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
     marks: optional list; (phase name, CUDA event) pairs are appended at the phase
     boundaries (tools/time_dist.py).
     fused: scatter straight into the owners' receive buffers over peer memory instead of
-    partition + all-to-all + regroup (module docstring); default: on for the NCCL backend.
-    peers: the object that provides those buffers (default SymmPeers(group)).
+    partition + all-to-all + regroup (module docstring).  Default: on when `peers` is given.
+    peers: the object that provides those buffers; pass SymmPeers(group, reuse=True) and keep
+    it between calls (fused=True alone allocates and exchanges fresh buffers in every call,
+    ~7 ms: safe, since the result owns its buffer, but slower than the all-to-all path).
     """
     import torch
     import torch.distributed as dist
@@ -290,7 +292,7 @@ def dist_sort(keys, k: int = 1024, base_case: int = 4096, seed: int = DEFAULT_SE
         model, status = attempt(lambda: ops.fit(smp, kt, k))          # step 2 (same on all ranks)
     mark("sample+fit")
     if fused is None:
-        fused = dist.get_backend(group) == "nccl"
+        fused = peers is not None
     if fused and model is not None and status == 0 and model.kind != MODEL_EQ3:
         return _fused_tail(keys, model, kt, k, base_case, seed, group, ops, peers, agree,
                            attempt, mark, cdev, G, r, gm)

@@ -132,6 +132,22 @@ def test_dist_sort_fused_one_rank_nccl(ipls, nccl1, kind, n):
     assert ref.bounds == res.bounds and ref.cuts == res.cuts
 
 
+def test_dist_sort_fused_reused_buffers(ipls, nccl1):
+    """SymmPeers(reuse=True): the receive buffer is kept while it is large enough and replaced
+    when it is not; every call's result is right while it is the latest."""
+    from paper_2208_06902_b200.distributed import SymmPeers, dist_sort
+    peers = SymmPeers(reuse=True)
+    rng = np.random.default_rng(5)
+    ptrs = []
+    for n in (200_000, 150_000, 900_000, 899_999):
+        a = rng.normal(0, 1, n)
+        res = dist_sort(dev(a).view(torch.float64), k=1024, base_case=4096, peers=peers)
+        assert res.keys.cpu().numpy().tobytes() == np.sort(a).tobytes()
+        ptrs.append(peers.buf.data_ptr())
+        assert res.keys.data_ptr() == peers.buf.data_ptr()
+    assert ptrs[0] == ptrs[1] and ptrs[2] == ptrs[3] and ptrs[1] != ptrs[2]
+
+
 def _model_of(ipls, r0, k):
     if r0.kind == oracle.MODEL_LINEAR:
         return ipls.Model(r0.A, r0.B, k, r0.D, ipls.MODEL_LINEAR, int(r0.capped), 0, False)
