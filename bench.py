@@ -375,9 +375,10 @@ def main():
                     help="keys of the workload the CPU oracle sorts for cpu_baseline")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--model", default="fmcd", choices=["fmcd", "tree"],
-                    help="partition model: fmcd (IPLS, the default and the headline) or tree "
-                         "(IPS4o's splitter tree on the same kernels, SURVEY NEXT #2)")
+    ap.add_argument("--model", default="fmcd", choices=["fmcd", "tree", "tree_eq"],
+                    help="partition model: fmcd (IPLS, the default and the headline), tree "
+                         "(IPS4o's splitter tree on the same kernels, SURVEY NEXT #2) or tree_eq "
+                         "(the tree with IPS4o's equality buckets)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: every rank sorts its own copy of the workload (weak scaling) "
                          "instead of dist_sort on one array sharded over the ranks")
@@ -413,7 +414,7 @@ def main():
     work = torch.empty_like(pristine)
     st = torch.cuda.current_stream()
 
-    model = ipls.MODEL_TREE if args.model == "tree" else ipls.MODEL_LINEAR
+    model = {"tree": ipls.MODEL_TREE, "tree_eq": ipls.MODEL_TREE_EQ}.get(args.model, ipls.MODEL_LINEAR)
     # L2 flush between the restore and the timed sort: a 256 MB write (> 126 MB L2) so that
     # no part of the restored input is L2-resident when the step starts
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)

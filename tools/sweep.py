@@ -82,7 +82,8 @@ def main():
             cfg = datagen.CONFIGS[name]
             a = datagen.generate(name)
             x = torch.from_numpy(a.view(np.int64)).cuda()
-            for model, mname in [(ipls.MODEL_LINEAR, "fmcd"), (ipls.MODEL_TREE, "tree")]:
+            for model, mname in [(ipls.MODEL_LINEAR, "fmcd"), (ipls.MODEL_TREE, "tree"),
+                                 (ipls.MODEL_TREE_EQ, "tree_eq")]:
                 r = run_case(x, a.dtype == np.float64, reps=10, k=cfg.k, base_case=cfg.base_case,
                              model=model)
                 res["models"][f"{name}/{mname}"] = r
