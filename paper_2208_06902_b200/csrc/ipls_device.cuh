@@ -15,6 +15,10 @@ namespace ipls {
 constexpr uint32_t kModelLinear = 0;
 constexpr uint32_t kModelEq3 = 1;
 constexpr uint32_t kModelTree = 2;   // splitter tree (IPS4o's classifier)
+// Bucketer MODE only (ModelDev.kind stays kModelTree; leaves != k selects it per chunk): the
+// tree with equality buckets (R24).  Its own instantiation, so that the plain tree's loops keep
+// their code (a run-time flag inside one instantiation cost the plain tree 4.5 % on C2).
+constexpr uint32_t kModelTreeEq = 3;
 constexpr uint32_t kSegForceEq3 = 1u;
 constexpr uint64_t kDstUserBit = 1ull << 63;  // seg_dst encoding: buffer select
 constexpr uint32_t kInhBit = 1u << 31;        // count word: child not homogeneous
@@ -115,13 +119,11 @@ struct Bucketer {
   const uint64_t* top;
   int depth;
   uint32_t leaves;
-  bool eqb;
   __device__ __forceinline__ explicit Bucketer(const ModelDev& md, uint32_t k)
       : A(md.A), B(md.B), piv(md.pivot_ok), km1(k - 1), heap(md.heap), top(md.top), depth(0),
-        leaves(k), eqb(false) {
-    if constexpr (MODE == (int)kModelTree) {
+        leaves(k) {
+    if constexpr (MODE == (int)kModelTree || MODE == (int)kModelTreeEq) {
       leaves = md.leaves;
-      eqb = md.leaves != k;
       while ((2u << depth) <= leaves) ++depth;  // log2 leaves (a power of two)
     }
   }
@@ -133,11 +135,13 @@ struct Bucketer {
       const uint64_t o = ok_of<F64>(bits);
       uint32_t j = 1;
       const int dt = depth < 8 ? depth : 8;
-      if (!eqb) {
-        for (int d = 0; d < dt; ++d) j = 2 * j + (o > top[j] ? 1u : 0u);
-        for (int d = dt; d < depth; ++d) j = 2 * j + (o > __ldg(heap + j) ? 1u : 0u);
-        return j - leaves;
-      }
+      for (int d = 0; d < dt; ++d) j = 2 * j + (o > top[j] ? 1u : 0u);
+      for (int d = dt; d < depth; ++d) j = 2 * j + (o > __ldg(heap + j) ? 1u : 0u);
+      return j - leaves;
+    } else if constexpr (MODE == (int)kModelTreeEq) {
+      const uint64_t o = ok_of<F64>(bits);
+      uint32_t j = 1;
+      const int dt = depth < 8 ? depth : 8;
       uint64_t last = ~o;  // splitter of the last left turn; != o while there was none
       for (int d = 0; d < dt; ++d) {
         const uint64_t s = top[j];

@@ -1223,10 +1223,14 @@ __global__ __launch_bounds__(kCThreads) void k_classify_scan(LevelArgs a) {
     __syncthreads();
   }
   int nan_seen = 0;
-  if (md.kind == kModelEq3)
+  if (md.kind == kModelEq3) {
     classify_dispatch<F64, kModelEq3>(a, ch, md, hist, nan_seen);
-  else
-    classify_dispatch<F64, TREE ? kModelTree : kModelLinear>(a, ch, md, hist, nan_seen);
+  } else if constexpr (TREE) {
+    if (md.leaves != k) classify_dispatch<F64, kModelTreeEq>(a, ch, md, hist, nan_seen);
+    else classify_dispatch<F64, kModelTree>(a, ch, md, hist, nan_seen);
+  } else {
+    classify_dispatch<F64, kModelLinear>(a, ch, md, hist, nan_seen);
+  }
   if (a.check_nan) {
     if (__syncthreads_or(nan_seen) && threadIdx.x == 0) atomicOr(a.err, kErrNan);
   } else {
@@ -1435,7 +1439,8 @@ __device__ void scatter_stable_chunk(const LevelArgs& a, uint64_t* __restrict__ 
                                      const ChunkDesc& ch, const ModelDev& md,
                                      unsigned char* smraw) {
   constexpr int NT = kSThreads;
-  constexpr bool kStageBucket = MODE == (int)kModelTree;  // a tree descent costs more than a load
+  constexpr bool kStageBucket =  // a tree descent costs more than a load
+      MODE == (int)kModelTree || MODE == (int)kModelTreeEq;
   const uint32_t k = a.k;
   uint64_t* stage = reinterpret_cast<uint64_t*>(smraw);              // kSTile keys
   uint16_t* sbk = reinterpret_cast<uint16_t*>(stage + kSTile);        // kSTile (tree only)
@@ -1889,6 +1894,8 @@ __global__ __launch_bounds__(kSThreads, 1) void k_scatter_stable(LevelArgs a, ui
   constexpr int kMain = TREE ? (int)kModelTree : (int)kModelLinear;
   if (md.kind == kModelEq3)
     scatter_stable_chunk<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw);
+  else if (TREE && md.leaves != a.k)
+    scatter_stable_chunk<F64, TREE ? (int)kModelTreeEq : kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
   else
     scatter_stable_chunk<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
 }
@@ -1920,6 +1927,8 @@ __global__ __launch_bounds__(kTThreads, 1) void k_scatter_term(LevelArgs a, uint
   constexpr int kMain = TREE ? (int)kModelTree : (int)kModelLinear;
   if (md.kind == kModelEq3)
     scatter_term_chunk<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw);
+  else if (TREE && md.leaves != a.k)
+    scatter_term_chunk<F64, TREE ? (int)kModelTreeEq : kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
   else
     scatter_term_chunk<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw);
 }
@@ -2627,6 +2636,9 @@ __global__ __launch_bounds__(kTThreads, 1) void k_term_fused(LevelArgs a, uint64
     constexpr int kMain = TREE ? (int)kModelTree : (int)kModelLinear;
     if (md.kind == kModelEq3)
       scatter_term_chunk<F64, kModelEq3>(a, dst_user, dst_scr, c, ch, md, smraw, next_ticket);
+    else if (TREE && md.leaves != k)
+      scatter_term_chunk<F64, TREE ? (int)kModelTreeEq : kMain>(a, dst_user, dst_scr, c, ch, md, smraw,
+                                                                next_ticket);
     else
       scatter_term_chunk<F64, kMain>(a, dst_user, dst_scr, c, ch, md, smraw, next_ticket);
     // this chunk's stores are visible before it counts; the last one reads them all

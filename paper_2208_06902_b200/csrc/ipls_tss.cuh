@@ -154,6 +154,9 @@ __global__ __launch_bounds__(kXThreads, 2) void k_tss_scatter(LevelArgs a, uint6
   constexpr int kMain = TREE ? (int)kModelTree : (int)kModelLinear;
   if (md.kind == kModelEq3)
     tss_scatter_chunk<F64, kModelEq3>(a, dst_user, dst_scr, blockIdx.x, ch, md, tw, smraw);
+  else if (TREE && md.leaves != a.k)
+    tss_scatter_chunk<F64, TREE ? (int)kModelTreeEq : kMain>(a, dst_user, dst_scr, blockIdx.x, ch, md, tw,
+                                                            smraw);
   else
     tss_scatter_chunk<F64, kMain>(a, dst_user, dst_scr, blockIdx.x, ch, md, tw, smraw);
 }
