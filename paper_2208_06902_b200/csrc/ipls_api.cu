@@ -651,8 +651,9 @@ ipls_status run_sort(uint64_t* keys, const Params& p, void* fixed, void* d_meta_
     // larger segments (skewed inputs: C3, C5, the paper's mixture and Zipf) the fused kernel's
     // per-CTA base-case phases balance worse than the separate launches (C3 -1.2 %, C5 -1.4 %,
     // mixture -2.7 %, Zipf -2.8 % separate; C2 -2.1 % fused)
+    // The splitter tree keeps the separate kernels too (C2 / C3 / C5 -1.5 to -2 % separate).
     la.fused_term = (level_keys / std::max<uint32_t>(nseg, 1) >= 32768u &&
-                     max_S <= sample_size(1ull << 20, k)) ? 1u : 0u;
+                     max_S <= sample_size(1ull << 20, k) && !p.tree) ? 1u : 0u;
     if (g_term_mode.load() == 1) la.fused_term = 1;
     if (g_term_mode.load() == 2) la.fused_term = 0;
     // Terminal segments sorted by windows (ipls_tss.cuh) unless a test hook asks for the

@@ -17,7 +17,7 @@ for name in names:
         for r in range(8):
             t.copy_(src); torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(); ipls.sort(t, k=1024, base_case=4096, key_type=kt); e1.record(); torch.cuda.synchronize()
+            e0.record(); ipls.sort(t, k=1024, base_case=4096, key_type=kt, model=int(os.environ.get("MODEL", "0"))); e1.record(); torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         row.append(f"mode{mode} {np.median(ts[2:]):.3f}")
     ipls.lib().ipls_debug_term_mode(0)
