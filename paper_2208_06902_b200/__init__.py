@@ -18,7 +18,8 @@ import numpy as np
 __all__ = [
     "IPLSError", "lib", "sort", "sort_host", "sort_host_batch", "fit_fmcd", "partition_level", "sort_trace",
     "workspace_bytes", "Model", "Record", "KEY_F64", "KEY_U64", "MODEL_LINEAR", "MODEL_EQ3", "MODEL_TREE",
-    "DEFAULT_SEED", "launch_count", "sample_size", "sample_strata", "assign_ranges", "assign_cuts",
+    "MODEL_TREE_EQ", "DEFAULT_SEED", "launch_count", "sample_size", "sample_strata", "assign_ranges",
+    "assign_cuts", "partition_count", "partition_scatter_to", "regroup_runs", "sort_segments",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
