@@ -35,23 +35,28 @@ def digests(records):
 
 
 def main():
-    # usage: make_oracle_digests.py [--tree] [cfg ...]; --tree: the splitter-tree model
-    # (IPLS_FLAG_TREE_MODEL, R22-R24) into oracle_digests_tree.txt
+    # usage: make_oracle_digests.py [--tree | --tree-eq] [cfg ...]; --tree: the splitter-tree
+    # model (IPLS_FLAG_TREE_MODEL, R22-R23) into oracle_digests_tree.txt; --tree-eq: the tree
+    # with equality buckets (R24) into oracle_digests_tree_eq.txt
     args = sys.argv[1:]
     tree = "--tree" in args
-    args = [x for x in args if x != "--tree"]
+    tree_eq = "--tree-eq" in args
+    args = [x for x in args if x not in ("--tree", "--tree-eq")]
     names = args or list(datagen.CONFIGS)
-    fname = "oracle_digests_tree.txt" if tree else "oracle_digests.txt"
+    fname = ("oracle_digests_tree_eq.txt" if tree_eq else
+             "oracle_digests_tree.txt" if tree else "oracle_digests.txt")
+    flag = " --tree-eq" if tree_eq else " --tree" if tree else ""
+    model = (oracle.MODEL_TREE_EQ if tree_eq else oracle.MODEL_TREE if tree
+             else oracle.MODEL_LINEAR)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), fname)
-    lines = [f"# Written by tests/golden/make_oracle_digests.py{' --tree' if tree else ''} "
+    lines = [f"# Written by tests/golden/make_oracle_digests.py{flag} "
              "(oracle/ only; seed 0x49504C53).",
              "# LEVEL cfg level n_records records_sha counts_sha samples_sha",
              "# FINAL cfg levels final_sha256"]
     for name in names:
         cfg = datagen.CONFIGS[name]
         a = datagen.generate(name)
-        r = oracle.sort(a, k=cfg.k, base_case=cfg.base_case, trace=True,
-                        model=oracle.MODEL_TREE if tree else oracle.MODEL_LINEAR)
+        r = oracle.sort(a, k=cfg.k, base_case=cfg.base_case, trace=True, model=model)
         assert r.status == 0
         for lv, nrec, d1, d2, d3 in digests(r.records):
             lines.append(f"LEVEL {name} {lv} {nrec} {d1} {d2} {d3}")

@@ -462,6 +462,22 @@ def test_tree_configs_full_size_vs_oracle_digests(ipls, name):
     assert hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest() == fin[name][1]
 
 
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_tree_eq_configs_full_size_vs_oracle_digests(ipls, name):
+    """The tree with equality buckets (R24) at full BASELINE sizes against oracle-written
+    digests (tests/golden/oracle_digests_tree_eq.txt)."""
+    lvd, fin = load_oracle_digests("oracle_digests_tree_eq.txt")
+    cfg = datagen.CONFIGS[name]
+    a = datagen.generate(name)
+    t = dev(a)
+    del a
+    gtr = ipls.sort_trace(t, k=cfg.k, base_case=cfg.base_case,
+                          key_type=kt_of(datagen.generate(name, 1)), model=ipls.MODEL_TREE_EQ)
+    assert gpu_digests(gtr.records) == lvd[name]
+    assert gtr.levels == fin[name][0]
+    assert hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest() == fin[name][1]
+
+
 def _mix_sum(t, step=1 << 28):
     """Order-independent multiset digest: wrapping sum of a SplitMix64-style mix of every key
     (int64 arithmetic on the GPU, in slices to bound the temporaries)."""
